@@ -1,0 +1,225 @@
+/*
+ * tcse.h — C ABI of the B200-native ternary-CSE search path.
+ *
+ * This is the ONLY way host code reaches the CUDA kernels.  Every entry point
+ * replaces one function of the reference's header-only C++ library
+ * (/root/reference/proj/include/terncse/, "terncse"); the citation next to each
+ * declaration names the function it stands in for.  The reference has no
+ * plugin/FFI layer of its own, so the seam is the function
+ * contract of optimize_system / optimize_scheme; include/tcse/terncse_gpu.hpp
+ * is the C++ adapter a maintainer drops into the reference, and INTEGRATION.md
+ * shows the ctypes / C++ bindings.
+ *
+ * Conventions (all mirror the reference):
+ *   - variable ids are signed and 1-based (+i = coefficient +1 on x_i,
+ *     linear_system.hpp:63-65); fresh variable t gets id n_x + t
+ *     (linear_system.hpp:72-75);
+ *   - a pair is (i, j, rel_sign) with i < j, meaning x_i + rel_sign*x_j
+ *     (CanonicalPair, linear_system.hpp:20-28); canonical order is
+ *     (i, j, '+' before '-') (linear_system.hpp:30-36);
+ *   - every call is synchronous; buffers are caller-allocated; no
+ *     library-owned heap crosses the ABI;
+ *   - return 0 on success or a negative TCSE_E* code; tcse_last_error()
+ *     (thread-local) carries the reference's message text where one exists
+ *     ("search config: ...", "replay_prefix: unreplayable pair at position N",
+ *     parallel_search.hpp:117-140, cse_engine.hpp:53).
+ *
+ * Results never depend on the device, the number of devices or any execution
+ * knob: slots are keyed by (master_seed, salt, iteration, GLOBAL process id)
+ * exactly as assign_strategies does (parallel_search.hpp:172-208), and every
+ * process replays the reference's std::mt19937_64 stream bit-for-bit.
+ */
+#ifndef TCSE_H
+#define TCSE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCSE_ABI_VERSION 1
+
+/* error codes */
+enum {
+    TCSE_OK = 0,
+    TCSE_EINVAL = -1,    /* bad argument / config ("search config: ...") */
+    TCSE_EREPLAY = -2,   /* replay_prefix: unreplayable pair (cse_engine.hpp:50-54) */
+    TCSE_ECAPACITY = -3, /* caller buffer or device capacity too small */
+    TCSE_ECUDA = -4,     /* CUDA runtime error or no device */
+    TCSE_ENCCL = -5,     /* multi-rank exchange failed */
+    TCSE_EVERIFY = -6    /* optimize_scheme: internal verification failed (parallel_search.hpp:332-333) */
+};
+
+/* StrategyKind, same order and values (strategies.hpp:13-21) */
+enum {
+    TCSE_GREEDY = 0,
+    TCSE_GREEDY_ALTERNATIVE = 1,
+    TCSE_WEIGHTED_RANDOM = 2,
+    TCSE_GREEDY_RANDOM = 3,
+    TCSE_GREEDY_INTERSECTIONS = 4,
+    TCSE_MIXED = 5,
+    TCSE_GREEDY_POTENTIAL = 6,
+    TCSE_STRATEGY_COUNT = 7
+};
+
+/* CanonicalPair (linear_system.hpp:22-28) */
+typedef struct tcse_pair {
+    int32_t i;
+    int32_t j;
+    int32_t rel_sign; /* +1 or -1 */
+} tcse_pair;
+
+/* PairCount (linear_system.hpp:125-128) */
+typedef struct tcse_pair_count {
+    tcse_pair pair;
+    int32_t count;
+} tcse_pair_count;
+
+/* LinearSystem without fresh definitions (linear_system.hpp:76-122), CSR:
+ * expression r holds terms[row_ptr[r] .. row_ptr[r+1]), signed 1-based ids in
+ * [1, n_x]; the same validation as the LinearSystem constructor applies. */
+typedef struct tcse_system {
+    int32_t n_x;
+    int32_t n_e;
+    const int32_t* row_ptr; /* n_e + 1 entries */
+    const int32_t* terms;
+} tcse_system;
+
+/* ProcessConfig (strategies.hpp:46-53) */
+typedef struct tcse_process_config {
+    int32_t strategy;
+    int32_t reserved;
+    double alpha;
+    double beta;
+    double p_greedy;
+    uint64_t seed;
+    double mix_weights[4]; /* gi, ga, gr, wr */
+} tcse_process_config;
+
+/* SearchConfig (parallel_search.hpp:44-53) minus flip mode and threads, plus
+ * two stop knobs that are not in the reference (0 = off).  Call
+ * tcse_default_search_config() to get the reference defaults. */
+typedef struct tcse_search_config {
+    int32_t n_processes; /* 0 = 256, as optimize_system does (parallel_search.hpp:224) */
+    int32_t patience;
+    double strategy_weights[TCSE_STRATEGY_COUNT];
+    double reinit_fraction;
+    uint64_t master_seed;
+    int32_t forced_strategy; /* -1 = none (draw from weights) */
+    int32_t max_iterations;  /* 0 = until patience (reference behaviour) */
+    double mix_weights[4];   /* ProcessConfig default {8,4,2,1} */
+} tcse_search_config;
+
+/* SolutionRecord (cse_engine.hpp:18-23).  subs is caller-allocated with room
+ * for cap pairs; cap >= naive_cost(system) always suffices because every
+ * substitution lowers the cost by at least one. */
+typedef struct tcse_record {
+    tcse_pair* subs;
+    int32_t cap;
+    int32_t n_subs;
+    int32_t cost;
+    int32_t strategy;
+    uint64_t seed;
+} tcse_record;
+
+/* execution counters (not part of any reference result) */
+typedef struct tcse_stats {
+    uint64_t steps;        /* selected substitutions (replayed prefixes excluded) */
+    uint64_t replayed;     /* prefix substitutions replayed by reinit processes */
+    uint64_t processes;    /* process runs */
+    uint64_t launches;     /* search-kernel launches */
+    int32_t iterations;    /* iteration barriers passed (max over systems) */
+    int32_t reserved;
+    double kernel_ms;      /* summed search-kernel time (CUDA events) */
+    double wall_ms;        /* whole call */
+    double exchange_ms;    /* reduce + cross-rank exchange time */
+} tcse_stats;
+
+/* Called on the calling thread after every iteration barrier, like
+ * optimize_system's on_iteration (parallel_search.hpp:222, 267-268).  A
+ * nonzero return stops the search at this barrier (fixed wall-time budgets). */
+typedef int (*tcse_iter_cb)(int32_t system_index, int32_t iteration,
+                            const tcse_record* incumbent, void* user);
+
+/* Multi-rank exchange: all-gather of `bytes` bytes from every rank into
+ * recv (world * bytes, rank-major).  Returns 0 on success. */
+typedef int (*tcse_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
+
+typedef struct tcse_ctx tcse_ctx;
+
+const char* tcse_last_error(void);
+int32_t tcse_abi_version(void);
+int32_t tcse_device_count(void);
+
+/* reference defaults: weights {0,4,1,2,8,0.1,0.01}, reinit 0.40, patience 10,
+ * seed 0, no forced strategy (parallel_search.hpp:31-53) */
+void tcse_default_search_config(tcse_search_config* cfg);
+
+/* upper bound on record length for a system (= its naive cost) */
+int32_t tcse_naive_cost(const tcse_system* sys);
+
+/* Owns the device, its stream, device pools and (optionally) the rank
+ * partition.  NULL on failure (see tcse_last_error). */
+tcse_ctx* tcse_create(int32_t device);
+void tcse_destroy(tcse_ctx* ctx);
+
+/* Process partition across ranks: this rank runs global process ids
+ * [floor(p*rank/world) ...) of every iteration; allgather exchanges the
+ * per-iteration costs and local best records.  world = 1 (default) needs no
+ * allgather.  The result is identical for every world size. */
+int tcse_set_partition(tcse_ctx* ctx, int32_t rank, int32_t world,
+                       tcse_allgather_fn allgather, void* user);
+
+/* count_pairs (linear_system.hpp:151-161) of the state replay_prefix(sys,
+ * prefix) (cse_engine.hpp:47-57), computed on the device.  min_count = 1
+ * returns every pair by popcount of the occurrence masks; min_count = 2
+ * returns the kernel's incrementally maintained candidate list
+ * (PairStats::candidates, linear_system.hpp:141-148).  Output in canonical
+ * order; *n_out = number of pairs (may exceed cap -> TCSE_ECAPACITY). */
+int tcse_count_pairs(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
+                     int32_t n_prefix, int32_t min_count, tcse_pair_count* out,
+                     int32_t cap, int32_t* n_out);
+
+/* n independent run_cse calls (cse_engine.hpp:29-43) in one launch:
+ * process b runs `std::mt19937_64 rng(cfgs[b].seed); run_cse(replay_prefix(
+ * sys, prefix), cfgs[b], rng)`.  out[b].subs receives only the substitutions
+ * run_cse selected (the prefix is not repeated); out[b].cost is total_cost of
+ * the final state.  trace (optional, n * trace_stride entries): per process,
+ * the FNV-1a-64 hash of the candidate list (pair, count) seen at each step,
+ * in canonical order, as the oracle computes it. */
+int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
+                 int32_t n_prefix, const tcse_process_config* cfgs, int32_t n,
+                 tcse_record* out, uint64_t* trace, int32_t trace_stride,
+                 tcse_stats* stats);
+
+/* optimize_system (parallel_search.hpp:220-273): portfolio search over one
+ * expression set.  best receives the incumbent record (prefix included),
+ * *iterations the iteration count of SystemSearchResult. */
+int tcse_optimize_system(tcse_ctx* ctx, const tcse_system* sys, const tcse_search_config* cfg,
+                         uint64_t stream_salt, tcse_iter_cb cb, void* user,
+                         tcse_record* best, int32_t* iterations, tcse_stats* stats);
+
+/* n_systems independent optimize_system calls run CONCURRENTLY in shared
+ * launches (system s uses stream salt salts[s]); result s is identical to
+ * tcse_optimize_system(systems[s], cfg, salts[s]).  optimize_scheme runs U, V
+ * and W this way instead of sequentially (parallel_search.hpp:329-341). */
+int tcse_optimize_systems(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
+                          const tcse_search_config* cfg, const uint64_t* salts,
+                          tcse_iter_cb cb, void* user, tcse_record* best,
+                          int32_t* iterations, tcse_stats* stats);
+
+/* Host-side result/verification API kept from the reference (no GPU):
+ * replay_prefix + total_cost + expand_and_verify (linear_system.hpp:193-258,
+ * cse_engine.hpp:47-57).  Returns 1 if the record replays, its cost matches
+ * *cost_out (written) and the expansion equals the original, 0 if not, <0 on
+ * a replay error. */
+int tcse_verify_record(const tcse_system* sys, const tcse_pair* subs, int32_t n_subs,
+                       int32_t* cost_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCSE_H */
