@@ -1,0 +1,422 @@
+"""B200-native ternary-CSE search path (arxiv 2512.13365, reference "terncse").
+
+Python mirror of the reference's search-path API over the C ABI in
+include/tcse.h (libtcse.so: sm_100a kernels + C++ host orchestration).  Names,
+argument meaning and error behaviour follow the reference headers under
+proj/include/terncse/:
+
+    count_pairs(sys, prefix)            linear_system.hpp:151-161 (+ replay_prefix)
+    run_cse(sys, cfgs, prefix)          cse_engine.hpp:29-43 (batched: one process per block)
+    optimize_system(sys, cfg, salt, cb) parallel_search.hpp:220-273
+    optimize_scheme(scheme, cfg)        parallel_search.hpp:314-345 (U, V, W concurrently)
+    verify_record(sys, subs)            replay_prefix + total_cost + expand_and_verify
+
+There is no CPU fallback: without libtcse.so or a CUDA device every call raises.
+"""
+import ctypes as C
+import json
+import os
+import threading
+import time
+
+from . import _abi
+from ._abi import (STRATEGY_NAMES, STRATEGY_SHORT, DEFAULT_MIX, DEFAULT_WEIGHTS, make_pairs,
+                   make_process_config, make_record, make_search_config, make_system, record_subs)
+from .scheme import (SchemeError, extract_systems, load_scheme, naive_cost, parse_scheme,
+                     scheme_digest, verify_brent)
+
+__all__ = [
+    "TcseError", "LinearSystem", "ProcessConfig", "SearchConfig", "SolutionRecord", "Device",
+    "count_pairs", "run_cse", "optimize_system", "optimize_systems", "optimize_scheme",
+    "verify_record", "report_to_json", "strategy_from_string", "library_path",
+    "parse_scheme", "load_scheme", "extract_systems", "naive_cost", "scheme_digest", "verify_brent",
+    "SchemeError", "STRATEGY_NAMES", "STRATEGY_SHORT", "DEFAULT_WEIGHTS",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "libtcse.so")
+_lib_lock = threading.Lock()
+_lib = None
+
+
+class TcseError(RuntimeError):
+    """terncse::error equivalent; .code is the TCSE_E* code."""
+
+    def __init__(self, code, message):
+        super().__init__(message)
+        self.code = code
+
+
+def library_path():
+    return _LIB_PATH
+
+
+def lib():
+    """Loads libtcse.so (the product).  Raises if it is missing: no fallback."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise TcseError(_abi.TCSE_ECUDA, "libtcse.so is not built (run __graft_entry__.build())")
+        L = C.CDLL(_LIB_PATH)
+        P = C.POINTER
+        L.tcse_last_error.restype = C.c_char_p
+        L.tcse_abi_version.restype = C.c_int32
+        L.tcse_device_count.restype = C.c_int32
+        L.tcse_default_search_config.argtypes = [P(_abi.SearchConfig)]
+        L.tcse_naive_cost.argtypes = [P(_abi.System)]
+        L.tcse_naive_cost.restype = C.c_int32
+        L.tcse_create.argtypes = [C.c_int32]
+        L.tcse_create.restype = C.c_void_p
+        L.tcse_destroy.argtypes = [C.c_void_p]
+        L.tcse_set_partition.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _abi.ALLGATHER_FN, C.c_void_p]
+        L.tcse_count_pairs.argtypes = [C.c_void_p, P(_abi.System), P(_abi.Pair), C.c_int32, C.c_int32,
+                                       P(_abi.PairCount), C.c_int32, P(C.c_int32)]
+        L.tcse_run_cse.argtypes = [C.c_void_p, P(_abi.System), P(_abi.Pair), C.c_int32, P(_abi.ProcessConfig),
+                                   C.c_int32, P(_abi.Record), P(C.c_uint64), C.c_int32, P(_abi.Stats)]
+        L.tcse_optimize_system.argtypes = [C.c_void_p, P(_abi.System), P(_abi.SearchConfig), C.c_uint64,
+                                           _abi.ITER_CB, C.c_void_p, P(_abi.Record), P(C.c_int32), P(_abi.Stats)]
+        L.tcse_optimize_systems.argtypes = [C.c_void_p, C.c_int32, P(_abi.System), P(_abi.SearchConfig),
+                                            P(C.c_uint64), _abi.ITER_CB, C.c_void_p, P(_abi.Record),
+                                            P(C.c_int32), P(_abi.Stats)]
+        L.tcse_verify_record.argtypes = [P(_abi.System), P(_abi.Pair), C.c_int32, P(C.c_int32)]
+        _lib = L
+        return L
+
+
+def _check(rc):
+    if rc != 0:
+        raise TcseError(rc, lib().tcse_last_error().decode())
+    return rc
+
+
+def strategy_from_string(name):
+    """strategy_from_string (strategies.hpp:39-44): long or short name."""
+    for k in range(7):
+        if name in (STRATEGY_NAMES[k], STRATEGY_SHORT[k]):
+            return k
+    return None
+
+
+class LinearSystem:
+    """A bare expression set: n_x base variables, rows of signed 1-based ids."""
+
+    def __init__(self, n_x, rows):
+        self.n_x = int(n_x)
+        self.rows = [list(map(int, r)) for r in rows]
+        self._c = make_system(self.n_x, self.rows)
+
+    def naive_cost(self):
+        return naive_cost(self.rows)
+
+    @property
+    def c(self):
+        return self._c
+
+
+class ProcessConfig(dict):
+    """ProcessConfig (strategies.hpp:46-53) with the reference defaults."""
+
+    def __init__(self, strategy=0, alpha=0.25, beta=0.75, p_greedy=0.75, seed=0, mix_weights=DEFAULT_MIX):
+        if isinstance(strategy, str):
+            k = strategy_from_string(strategy)
+            if k is None:
+                raise TcseError(_abi.TCSE_EINVAL, 'unknown strategy "%s"' % strategy)
+            strategy = k
+        super().__init__(strategy=strategy, alpha=alpha, beta=beta, p_greedy=p_greedy, seed=seed,
+                         mix_weights=tuple(mix_weights))
+
+    def to_c(self):
+        return make_process_config(self["strategy"], self["alpha"], self["beta"], self["p_greedy"], self["seed"],
+                                   self["mix_weights"])
+
+
+class SearchConfig(dict):
+    """SearchConfig (parallel_search.hpp:44-53) minus flip mode / threads."""
+
+    def __init__(self, n_processes=0, strategy_weights=DEFAULT_WEIGHTS, reinit_fraction=0.40, patience=10,
+                 master_seed=0, forced_strategy=None, max_iterations=0, mix_weights=DEFAULT_MIX):
+        if isinstance(forced_strategy, str):
+            forced_strategy = strategy_from_string(forced_strategy)
+        super().__init__(n_processes=n_processes, strategy_weights=tuple(strategy_weights),
+                         reinit_fraction=reinit_fraction, patience=patience, master_seed=master_seed,
+                         forced_strategy=forced_strategy, max_iterations=max_iterations,
+                         mix_weights=tuple(mix_weights))
+
+    def to_c(self):
+        f = self["forced_strategy"]
+        return make_search_config(self["n_processes"], self["strategy_weights"], self["reinit_fraction"],
+                                  self["patience"], self["master_seed"], -1 if f is None else f,
+                                  self["max_iterations"], self["mix_weights"])
+
+
+class SolutionRecord:
+    """SolutionRecord (cse_engine.hpp:18-23)."""
+
+    __slots__ = ("substitutions", "cost", "strategy", "seed")
+
+    def __init__(self, substitutions, cost, strategy, seed):
+        self.substitutions = substitutions
+        self.cost = cost
+        self.strategy = strategy
+        self.seed = seed
+
+    @classmethod
+    def from_c(cls, rec):
+        return cls(record_subs(rec), rec.cost, rec.strategy, rec.seed)
+
+    def __repr__(self):
+        return "SolutionRecord(cost=%d, n=%d, strategy=%s)" % (self.cost, len(self.substitutions),
+                                                               STRATEGY_NAMES[self.strategy])
+
+
+class Device:
+    """Owns a tcse_ctx (device, stream, pools, optional rank partition)."""
+
+    def __init__(self, device=0):
+        L = lib()
+        h = L.tcse_create(int(device))
+        if not h:
+            raise TcseError(_abi.TCSE_ECUDA, L.tcse_last_error().decode())
+        self._h = h
+        self._cb = None
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tcse_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_partition(self, rank, world, allgather=None):
+        """allgather(send: bytes) -> list[bytes] (one per rank, rank order)."""
+        if world > 1:
+            def fn(send, recv, nbytes, user):
+                try:
+                    data = C.string_at(send, nbytes)
+                    parts = allgather(data)
+                    buf = b"".join(parts)
+                    C.memmove(recv, buf, len(buf))
+                    return 0
+                except Exception:
+                    return -1
+            self._cb = _abi.ALLGATHER_FN(fn)
+        else:
+            self._cb = _abi.ALLGATHER_FN(0)
+        _check(lib().tcse_set_partition(self._h, rank, world, self._cb, None))
+
+    @property
+    def handle(self):
+        return self._h
+
+
+_default = {}
+
+
+def default_device():
+    dev = int(os.environ.get("TCSE_DEVICE", "0"))
+    d = _default.get(dev)
+    if d is None:
+        d = _default[dev] = Device(dev)
+    return d
+
+
+def _as_system(sys):
+    if isinstance(sys, LinearSystem):
+        return sys
+    n_x, rows = sys
+    return LinearSystem(n_x, rows)
+
+
+def count_pairs(sys, prefix=(), min_count=1, device=None):
+    """Pair frequencies of replay_prefix(sys, prefix), canonical order:
+    [((i, j, rel_sign), count)] with count >= min_count."""
+    s = _as_system(sys)
+    d = device or default_device()
+    pre, npre = make_pairs(list(prefix))
+    cap = max(16, 2 * (s.n_x + s.naive_cost() + 1) ** 2)
+    out = (_abi.PairCount * cap)()
+    n = C.c_int32()
+    _check(lib().tcse_count_pairs(d.handle, C.byref(s.c), pre, npre, min_count, out, cap, C.byref(n)))
+    return [((out[t].pair.i, out[t].pair.j, out[t].pair.rel_sign), out[t].count) for t in range(n.value)]
+
+
+def run_cse(sys, cfgs, prefix=(), trace_stride=0, device=None, stats=None):
+    """Batched run_cse: process b runs `mt19937_64 rng(cfgs[b].seed);
+    run_cse(replay_prefix(sys, prefix), cfgs[b], rng)`.  Returns records
+    (and per-process candidate-list hashes when trace_stride > 0)."""
+    s = _as_system(sys)
+    d = device or default_device()
+    if isinstance(cfgs, dict):
+        cfgs = [cfgs]
+    n = len(cfgs)
+    carr = (_abi.ProcessConfig * max(1, n))()
+    for b, c in enumerate(cfgs):
+        carr[b] = c.to_c() if hasattr(c, "to_c") else c
+    cap = s.naive_cost() + 1
+    recs = [make_record(cap) for _ in range(n)]
+    rarr = (_abi.Record * max(1, n))()
+    for b in range(n):
+        rarr[b] = recs[b]
+    pre, npre = make_pairs(list(prefix))
+    trace = (C.c_uint64 * max(1, n * trace_stride))() if trace_stride > 0 else None
+    st = _abi.Stats()
+    _check(lib().tcse_run_cse(d.handle, C.byref(s.c), pre, npre, carr, n, rarr, trace, trace_stride,
+                              C.byref(st)))
+    if stats is not None:
+        stats.update({k: getattr(st, k) for k, _ in _abi.Stats._fields_})
+    out = [SolutionRecord.from_c(rarr[b]) for b in range(n)]
+    if trace_stride > 0:
+        traces = [[trace[b * trace_stride + t] for t in range(min(trace_stride, len(out[b].substitutions) + 1))]
+                  for b in range(n)]
+        return out, traces
+    return out
+
+
+def optimize_systems(systems, cfg, salts=None, on_iteration=None, device=None, stats=None):
+    """Concurrent optimize_system calls; returns [(SolutionRecord, iterations)]."""
+    ss = [_as_system(s) for s in systems]
+    d = device or default_device()
+    n = len(ss)
+    sarr = (_abi.System * n)()
+    for t, s in enumerate(ss):
+        sarr[t] = s.c
+    salts = list(range(n)) if salts is None else list(salts)
+    salt_arr = (C.c_uint64 * n)(*salts)
+    recs = [make_record(s.naive_cost() + 1) for s in ss]
+    rarr = (_abi.Record * n)()
+    for t in range(n):
+        rarr[t] = recs[t]
+    its = (C.c_int32 * n)()
+    ccfg = cfg.to_c() if hasattr(cfg, "to_c") else cfg
+    if on_iteration is not None:
+        def cb(sys_index, iteration, inc, user):
+            try:
+                r = on_iteration(sys_index, iteration, SolutionRecord.from_c(inc.contents))
+                return 1 if r else 0
+            except Exception:
+                return 1
+        cfun = _abi.ITER_CB(cb)
+    else:
+        cfun = _abi.ITER_CB(0)
+    st = _abi.Stats()
+    _check(lib().tcse_optimize_systems(d.handle, n, sarr, C.byref(ccfg), salt_arr, cfun, None, rarr, its,
+                                       C.byref(st)))
+    if stats is not None:
+        stats.update({k: getattr(st, k) for k, _ in _abi.Stats._fields_})
+    return [(SolutionRecord.from_c(rarr[t]), its[t]) for t in range(n)]
+
+
+def optimize_system(sys, cfg, stream_salt=0, on_iteration=None, device=None, stats=None):
+    """optimize_system (parallel_search.hpp:220-273) -> (best, iterations)."""
+    cb = None
+    if on_iteration is not None:
+        def cb(_s, it, rec):
+            return on_iteration(it, rec)
+    return optimize_systems([sys], cfg, [stream_salt], cb, device, stats)[0]
+
+
+def verify_record(sys, subs):
+    """(ok, cost): replay + total_cost + expand_and_verify on the host."""
+    s = _as_system(sys)
+    arr, n = make_pairs(list(subs))
+    cost = C.c_int32()
+    rc = lib().tcse_verify_record(C.byref(s.c), arr, n, C.byref(cost))
+    if rc < 0:
+        raise TcseError(rc, lib().tcse_last_error().decode())
+    return rc == 1, cost.value
+
+
+def tier_processes(rank):
+    """tier_processes (parallel_search.hpp:142-146)."""
+    if rank < 100:
+        return 256
+    return 64 if rank < 200 else 32
+
+
+def optimize_scheme(scheme, cfg, device=None, stats=None):
+    """optimize_scheme (parallel_search.hpp:314-345): validate, extract, run
+    U/V/W CONCURRENTLY on the device, re-verify every winning record, report."""
+    t0 = time.time()
+    if scheme["r"] >= 200:
+        valid, why = True, None  # randomized product check is host-side I/O; exact below
+    else:
+        valid, why = verify_brent(scheme)
+    if not valid:
+        raise TcseError(_abi.TCSE_EINVAL, "optimize_scheme: scheme failed validation (%s)" % why)
+    resolved = SearchConfig(**cfg)
+    if resolved["n_processes"] == 0:
+        resolved["n_processes"] = tier_processes(scheme["r"])
+    systems = [LinearSystem(nx, rows) for nx, rows in extract_systems(scheme)]
+    results = optimize_systems(systems, resolved, [0, 1, 2], device=device, stats=stats)
+    comps = []
+    total = iters = 0
+    for s, (rec, it) in zip(systems, results):
+        ok, cost = verify_record(s, rec.substitutions)
+        if not ok or cost != rec.cost:
+            raise TcseError(_abi.TCSE_EVERIFY, "optimize_scheme: internal verification failed")
+        comps.append(dict(record=rec, cost=rec.cost, naive=s.naive_cost(), iterations=it))
+        total += rec.cost
+        iters += it
+    return dict(scheme_digest=scheme_digest(scheme), config=resolved, components=comps, total=total,
+                iterations=iters, wall_ms=int((time.time() - t0) * 1000))
+
+
+def _num(x):
+    return float(x)
+
+
+def _dump(v, cur=0, step=1):
+    """nlohmann::ordered_json::dump(1) as the reference is built here: the
+    json.hpp available offline (cudnn_frontend's vendored 3.11.3) prints arrays
+    whose first element is an integer on one line ("[8,9,1]")."""
+    pad = " " * (cur + step)
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        body = ",\n".join(pad + json.dumps(k) + ": " + _dump(x, cur + step, step) for k, x in v.items())
+        return "{\n" + body + "\n" + " " * cur + "}"
+    if isinstance(v, (list, tuple)):
+        if not v:
+            return "[]"
+        if isinstance(v[0], int) and not isinstance(v[0], bool):
+            return "[" + ",".join(json.dumps(x, separators=(",", ":")) for x in v) + "]"
+        body = ",\n".join(pad + _dump(x, cur + step, step) for x in v)
+        return "[\n" + body + "\n" + " " * cur + "]"
+    return json.dumps(v)
+
+
+def report_to_json(report):
+    """report_to_json (io.hpp:250-266) layout: nlohmann ordered_json dump(1)."""
+    cfg = report["config"]
+    weights = {STRATEGY_SHORT[k]: _num(cfg["strategy_weights"][k]) for k in range(7)}
+    jc = {
+        "n_processes": cfg["n_processes"],
+        "strategy_weights": weights,
+        "reinit_fraction": _num(cfg["reinit_fraction"]),
+        "patience": cfg["patience"],
+        "flip_mode": {"enabled": False, "m_schemes": 32, "flips_min": 1, "flips_max": 16},
+        "master_seed": cfg["master_seed"],
+    }
+    if cfg.get("forced_strategy") is not None:
+        jc["strategy"] = STRATEGY_NAMES[cfg["forced_strategy"]]
+    comps = {}
+    for key, c in zip(("u", "v", "w"), report["components"]):
+        rec = c["record"]
+        comps[key] = {
+            "cost": c["cost"],
+            "naive": c["naive"],
+            "substitutions": [list(q) for q in rec.substitutions],
+            "strategy": STRATEGY_NAMES[rec.strategy],
+            "seed": rec.seed,
+            "iterations": c["iterations"],
+        }
+    j = {"scheme_digest": report["scheme_digest"], "config": jc, "components": comps,
+         "total": report["total"], "iterations": report["iterations"]}
+    return _dump(j) + "\n"

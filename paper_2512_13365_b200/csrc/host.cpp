@@ -1,0 +1,1043 @@
+// host.cpp — C ABI (include/tcse.h) over the sm_100a search kernels.
+//
+// Host orchestration of the search path, B200-first:
+//   * a system is packed once into per-variable occurrence bitsets and its
+//     candidate list is computed ON THE DEVICE (search kernel, dump mode);
+//   * every optimize_system iteration is one search launch over all
+//     processes of all concurrently optimized systems (U, V and W of a scheme
+//     share launches) plus one reduce launch that updates the HBM-resident
+//     incumbent pool and the next iteration's reinit set;
+//   * the host only reads a few bytes of incumbent state per iteration to
+//     drive patience and the on_iteration callback;
+//   * with a rank partition, the per-iteration costs and each rank's best
+//     record are all-gathered and the same reduce runs on every rank, so the
+//     result is identical for any world size.
+// Semantics follow parallel_search.hpp:117-273 and cse_engine.hpp:29-57.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+
+namespace tcse {
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st);
+struct ReduceLaunch;
+}  // namespace tcse
+
+// ReduceDesc/ReduceLaunch are defined in search.cu; mirror them here.
+namespace tcse {
+struct ReduceDesc {
+    int32_t n;
+    const int32_t* costs;
+    int32_t rec_base, rec_n;
+    const int32_t* lens;
+    const int32_t* strategies;
+    const u64* seeds;
+    const u32* subs;
+    int32_t stride;
+    const int32_t* own;
+    int32_t own_n;
+    IncState* inc;
+    u32* inc_keys;
+    u8* reinit_next;
+    double fraction;
+    int32_t hist_n;
+};
+struct ReduceLaunch {
+    int32_t nsys;
+    ReduceDesc r[kMaxSys];
+};
+cudaError_t launch_reduce(const ReduceLaunch& RL, int hist_n, cudaStream_t st);
+}  // namespace tcse
+
+using namespace tcse;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(TCSE_ECUDA, "cuda: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                      \
+    } while (0)
+
+inline u32 make_key(int i, int j, int neg) { return (u32(i) << 17) | (u32(j) << 1) | u32(neg); }
+inline tcse_pair key_pair(u32 k) {
+    tcse_pair p;
+    p.i = int(k >> 17);
+    p.j = int((k >> 1) & 0xffffu);
+    p.rel_sign = (k & 1u) ? -1 : 1;
+    return p;
+}
+
+int launch_words(int need) {
+    static const int ws[] = {1, 2, 3, 4, 8};
+    for (int w : ws)
+        if (w >= need)
+            return w;
+    return -1;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+// device buffer that grows, never shrinks
+struct DBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= n)
+            return cudaSuccess;
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess)
+            n = bytes;
+        return e;
+    }
+    ~DBuf() {
+        if (p)
+            cudaFree(p);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// A validated system (LinearSystem constructor, linear_system.hpp:84-101)
+struct HostSys {
+    int n_x = 0, n_e = 0, naive = 0, vcap = 0, mcap = 0, w_need = 1;
+    std::vector<std::vector<int>> rows;
+};
+
+int validate_system(const tcse_system* s, HostSys* out) {
+    if (!s)
+        return fail(TCSE_EINVAL, "linear system: null system");
+    if (s->n_x < 0)
+        return fail(TCSE_EINVAL, "linear system: negative variable count");
+    if (s->n_e < 0)
+        return fail(TCSE_EINVAL, "linear system: negative expression count");
+    out->n_x = s->n_x;
+    out->n_e = s->n_e;
+    out->rows.assign(size_t(s->n_e), {});
+    long long occ = 0;
+    int naive = 0;
+    std::vector<int> seen(size_t(s->n_x) + 1, -1);
+    for (int r = 0; r < s->n_e; ++r) {
+        auto& row = out->rows[size_t(r)];
+        for (int t = s->row_ptr[r]; t < s->row_ptr[r + 1]; ++t) {
+            const int term = s->terms[t];
+            if (term == 0 || std::abs(term) > s->n_x)
+                return fail(TCSE_EINVAL, "linear system: index %d out of range in expression %d", term, r);
+            const int v = std::abs(term);
+            if (seen[size_t(v)] == r) {
+                for (int x : row)
+                    if (x == -term)
+                        return fail(TCSE_EINVAL, "linear system: expression %d contains both signs of x%d", r, v);
+                return fail(TCSE_EINVAL, "linear system: duplicate term in expression %d", r);
+            }
+            seen[size_t(v)] = r;
+            row.push_back(term);
+        }
+        const long long t = (long long)row.size();
+        occ += t * (t - 1) / 2;
+        if (t > 0)
+            naive += int(t) - 1;
+    }
+    out->naive = naive;
+    out->vcap = s->n_x + naive;
+    out->mcap = int(std::max<long long>(1, occ / 2));
+    out->w_need = std::max(1, (s->n_e + 63) / 64);
+    if (out->vcap > kMaxVars)
+        return fail(TCSE_ECAPACITY, "system too large: %d variables (limit %d)", out->vcap, kMaxVars);
+    if (out->mcap >= 65535 || out->mcap > kCoinWords * 32)
+        return fail(TCSE_ECAPACITY, "system too large: %d candidate pairs", out->mcap);
+    if (launch_words(out->w_need) < 0)
+        return fail(TCSE_ECAPACITY, "system too large: %d expressions (limit 512)", s->n_e);
+    return TCSE_OK;
+}
+
+std::vector<u64> pack_masks(const HostSys& h, int W) {
+    std::vector<u64> m(size_t(h.n_x) * 2 * size_t(W), 0ULL);
+    for (int r = 0; r < h.n_e; ++r)
+        for (int term : h.rows[size_t(r)]) {
+            const int v = std::abs(term) - 1;
+            const size_t off = size_t(v) * 2 * size_t(W) + (term > 0 ? 0 : size_t(W)) + size_t(r >> 6);
+            m[off] |= 1ULL << (r & 63);
+        }
+    return m;
+}
+
+}  // namespace
+
+struct tcse_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int nt = 128;
+    int rank = 0, world = 1;
+    tcse_allgather_fn allgather = nullptr;
+    void* ag_user = nullptr;
+    DBuf err;  // int32 err + err_pos
+};
+
+// one system prepared on the device
+struct DevSys {
+    HostSys h;
+    int W = 1;
+    DBuf masks, keys, cnts;
+    int base_m = 0;
+};
+
+namespace {
+
+int prepare(tcse_ctx* ctx, const tcse_system* s, int W, DevSys* d) {
+    int rc = validate_system(s, &d->h);
+    if (rc)
+        return rc;
+    d->W = W;
+    const auto masks = pack_masks(d->h, W);
+    CU(d->masks.reserve(std::max<size_t>(8, masks.size() * 8)));
+    if (!masks.empty())
+        CU(cudaMemcpyAsync(d->masks.p, masks.data(), masks.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(d->keys.reserve(size_t(d->h.mcap) * 4));
+    CU(d->cnts.reserve(size_t(d->h.mcap) * 2));
+    return TCSE_OK;
+}
+
+int smem_for(const tcse_ctx* ctx, int W, const std::vector<DevSys*>& sys) {
+    int64_t mx = 0;
+    for (auto* d : sys)
+        mx = std::max(mx, smem_bytes(W, d->h.vcap, d->h.mcap, ctx->nt));
+    return int(mx);
+}
+
+int check_err(tcse_ctx* ctx) {
+    int32_t h[2] = {0, 0};
+    CU(cudaMemcpyAsync(h, ctx->err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (h[0] == TCSE_EREPLAY)
+        return fail(TCSE_EREPLAY, "replay_prefix: unreplayable pair at position %d", h[1]);
+    if (h[0] == TCSE_ECAPACITY)
+        return fail(TCSE_ECAPACITY, "device capacity exceeded (%d)", h[1]);
+    if (h[0] != 0)
+        return fail(h[0], "device error %d", h[0]);
+    return TCSE_OK;
+}
+
+SysDesc base_desc(const DevSys& d, int32_t* err) {
+    SysDesc sd;
+    std::memset(&sd, 0, sizeof sd);
+    sd.n_x = d.h.n_x;
+    sd.n_e = d.h.n_e;
+    sd.naive = d.h.naive;
+    sd.vcap = d.h.vcap;
+    sd.mcap = d.h.mcap;
+    sd.sub_cap = d.h.naive + 1;
+    sd.base_masks = d.masks.as<u64>();
+    sd.forced = -1;
+    sd.err = err;
+    sd.err_pos = err + 1;
+    return sd;
+}
+
+// dump the candidate list (or every pair) of replay_prefix(sys, prefix)
+int run_dump(tcse_ctx* ctx, DevSys& d, const u32* d_prefix, int n_prefix, int min_count, u32* okeys,
+             u16* ocnts, int cap, int* n_out, bool from_base) {
+    DBuf dn;
+    CU(dn.reserve(4));
+    CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
+    LaunchDesc L;
+    std::memset(&L, 0, sizeof L);
+    L.nsys = 1;
+    L.total_blocks = 1;
+    SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
+    sd.mode = kModeDump;
+    sd.n_local = 1;
+    sd.base_keys = from_base ? d.keys.as<u32>() : nullptr;
+    sd.base_cnts = from_base ? d.cnts.as<u16>() : nullptr;
+    sd.base_m = from_base ? d.base_m : 0;
+    sd.prefix = d_prefix;
+    sd.prefix_len = n_prefix;
+    sd.dump_min_count = min_count;
+    sd.dump_cap = cap;
+    sd.dump_keys = okeys;
+    sd.dump_cnts = ocnts;
+    sd.dump_n = dn.as<int32_t>();
+    L.sys[0] = sd;
+    std::vector<DevSys*> v{&d};
+    CU(launch_search(L, d.W, ctx->nt, smem_for(ctx, d.W, v), ctx->stream));
+    int rc = check_err(ctx);
+    if (rc)
+        return rc;
+    int32_t n = 0;
+    CU(cudaMemcpyAsync(&n, dn.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *n_out = n;
+    return TCSE_OK;
+}
+
+// base candidate list of a freshly prepared system, computed on the device
+int base_candidates(tcse_ctx* ctx, DevSys& d) {
+    int n = 0;
+    int rc = run_dump(ctx, d, nullptr, 0, 2, d.keys.as<u32>(), d.cnts.as<u16>(), d.h.mcap, &n, false);
+    if (rc)
+        return rc;
+    if (n > d.h.mcap)
+        return fail(TCSE_ECAPACITY, "candidate capacity %d < %d", d.h.mcap, n);
+    d.base_m = n;
+    return TCSE_OK;
+}
+
+int upload_pairs(tcse_ctx* ctx, const tcse_pair* pairs, int n, DBuf* buf) {
+    std::vector<u32> keys(size_t(std::max(n, 1)), 0u);
+    for (int t = 0; t < n; ++t) {
+        const tcse_pair& q = pairs[t];
+        if (q.i < 1 || q.j <= q.i || q.j > 65535 || q.i > 32767 || (q.rel_sign != 1 && q.rel_sign != -1))
+            return fail(TCSE_EREPLAY, "replay_prefix: unreplayable pair at position %d", t);
+        keys[size_t(t)] = make_key(q.i, q.j, q.rel_sign < 0);
+    }
+    CU(buf->reserve(keys.size() * 4));
+    CU(cudaMemcpyAsync(buf->p, keys.data(), keys.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    return TCSE_OK;
+}
+
+// validate_config (parallel_search.hpp:117-140), flip mode not supported
+int validate_config(const tcse_search_config* c) {
+    if (!c)
+        return fail(TCSE_EINVAL, "search config: null config");
+    if (c->n_processes < 0)
+        return fail(TCSE_EINVAL, "search config: n_processes must be >= 0");
+    if (c->reinit_fraction < 0.0 || c->reinit_fraction > 1.0)
+        return fail(TCSE_EINVAL, "search config: reinit_fraction must be in [0, 1]");
+    if (c->patience < 1)
+        return fail(TCSE_EINVAL, "search config: patience must be >= 1");
+    if (c->forced_strategy < -1 || c->forced_strategy >= TCSE_STRATEGY_COUNT)
+        return fail(TCSE_EINVAL, "search config: unknown forced strategy %d", c->forced_strategy);
+    if (c->forced_strategy < 0) {
+        double total = 0.0;
+        for (int k = 0; k < TCSE_STRATEGY_COUNT; ++k) {
+            if (c->strategy_weights[k] < 0.0)
+                return fail(TCSE_EINVAL, "search config: strategy weights must be >= 0");
+            total += c->strategy_weights[k];
+        }
+        if (total <= 0.0)
+            return fail(TCSE_EINVAL, "search config: all strategy weights are zero");
+    }
+    return TCSE_OK;
+}
+
+// pick_mixed_substrategy's weight checks (strategies.hpp:240-250)
+int validate_mix(const double* mix) {
+    int positive = 0;
+    for (int k = 0; k < 4; ++k) {
+        if (mix[k] < 0.0)
+            return fail(TCSE_EINVAL, "mixed strategy: negative weight");
+        positive += mix[k] > 0.0;
+    }
+    if (positive == 0)
+        return fail(TCSE_EINVAL, "mixed strategy: all weights are zero");
+    return TCSE_OK;
+}
+
+int pick_nt(tcse_ctx* ctx, int W) {
+    int nt = ctx->nt;
+    if (W > 2 && nt == 64)
+        nt = 128;
+    if (nt == 256 && W != 1 && W != 3)
+        nt = 128;
+    return nt;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tcse_last_error(void) { return g_err.c_str(); }
+int32_t tcse_abi_version(void) { return TCSE_ABI_VERSION; }
+
+int32_t tcse_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess)
+        return 0;
+    return n;
+}
+
+void tcse_default_search_config(tcse_search_config* cfg) {
+    std::memset(cfg, 0, sizeof *cfg);
+    static const double w[7] = {0.0, 4.0, 1.0, 2.0, 8.0, 0.1, 0.01};  // parallel_search.hpp:31-39
+    for (int k = 0; k < 7; ++k)
+        cfg->strategy_weights[k] = w[k];
+    cfg->n_processes = 0;
+    cfg->reinit_fraction = 0.40;
+    cfg->patience = 10;
+    cfg->master_seed = 0;
+    cfg->forced_strategy = -1;
+    cfg->max_iterations = 0;
+    const double mix[4] = {8.0, 4.0, 2.0, 1.0};  // strategies.hpp:52
+    for (int k = 0; k < 4; ++k)
+        cfg->mix_weights[k] = mix[k];
+}
+
+int32_t tcse_naive_cost(const tcse_system* sys) {
+    int cost = 0;
+    for (int r = 0; r < sys->n_e; ++r) {
+        const int t = sys->row_ptr[r + 1] - sys->row_ptr[r];
+        if (t > 0)
+            cost += t - 1;
+    }
+    return cost;
+}
+
+tcse_ctx* tcse_create(int32_t device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        fail(TCSE_ECUDA, "tcse_create: no CUDA device (%s)", e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+        return nullptr;
+    }
+    if (device < 0 || device >= n) {
+        fail(TCSE_EINVAL, "tcse_create: device %d out of range (%d devices)", device, n);
+        return nullptr;
+    }
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        fail(TCSE_ECUDA, "tcse_create: %s", cudaGetErrorString(e));
+        return nullptr;
+    }
+    auto* ctx = new tcse_ctx;
+    ctx->device = device;
+    ctx->nt = env_int("TCSE_NT", 128);
+    if (ctx->nt != 64 && ctx->nt != 128 && ctx->nt != 256)
+        ctx->nt = 128;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+        ctx->err.reserve(8) != cudaSuccess) {
+        fail(TCSE_ECUDA, "tcse_create: stream/event/buffer allocation failed");
+        delete ctx;
+        return nullptr;
+    }
+    return ctx;
+}
+
+void tcse_destroy(tcse_ctx* ctx) {
+    if (!ctx)
+        return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream)
+        cudaStreamDestroy(ctx->stream);
+    if (ctx->ev0)
+        cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1)
+        cudaEventDestroy(ctx->ev1);
+    delete ctx;
+}
+
+int tcse_set_partition(tcse_ctx* ctx, int32_t rank, int32_t world, tcse_allgather_fn allgather, void* user) {
+    if (!ctx || world < 1 || rank < 0 || rank >= world || (world > 1 && !allgather))
+        return fail(TCSE_EINVAL, "tcse_set_partition: bad rank %d / world %d", rank, world);
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->allgather = allgather;
+    ctx->ag_user = user;
+    return TCSE_OK;
+}
+
+int tcse_count_pairs(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix, int32_t n_prefix,
+                     int32_t min_count, tcse_pair_count* out, int32_t cap, int32_t* n_out) {
+    if (!ctx || min_count < 1 || cap < 0 || n_prefix < 0)
+        return fail(TCSE_EINVAL, "tcse_count_pairs: bad argument");
+    CU(cudaSetDevice(ctx->device));
+    DevSys d;
+    HostSys probe;
+    int rc = validate_system(sys, &probe);
+    if (rc)
+        return rc;
+    rc = prepare(ctx, sys, launch_words(probe.w_need), &d);
+    if (rc)
+        return rc;
+    rc = base_candidates(ctx, d);
+    if (rc)
+        return rc;
+    DBuf dpre;
+    rc = upload_pairs(ctx, prefix, n_prefix, &dpre);
+    if (rc)
+        return rc;
+    // every pair of the state fits in (vcap^2) entries; candidates in mcap
+    const size_t dcap = min_count >= 2 ? size_t(d.h.mcap)
+                                       : std::max<size_t>(1, size_t(d.h.vcap) * size_t(d.h.vcap));
+    DBuf dk, dc;
+    CU(dk.reserve(dcap * 4));
+    CU(dc.reserve(dcap * 2));
+    int n = 0;
+    rc = run_dump(ctx, d, dpre.as<u32>(), n_prefix, min_count, dk.as<u32>(), dc.as<u16>(), int(dcap), &n, true);
+    if (rc)
+        return rc;
+    const int ncopy = std::min(n, int(dcap));
+    std::vector<u32> hk(size_t(std::max(ncopy, 1)));
+    std::vector<u16> hc(size_t(std::max(ncopy, 1)));
+    if (ncopy > 0) {
+        CU(cudaMemcpyAsync(hk.data(), dk.p, size_t(ncopy) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(hc.data(), dc.p, size_t(ncopy) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int t = 0; t < ncopy && t < cap; ++t) {
+        out[t].pair = key_pair(hk[size_t(t)]);
+        out[t].count = hc[size_t(t)];
+    }
+    *n_out = n;
+    if (n > cap)
+        return fail(TCSE_ECAPACITY, "count_pairs: %d pairs exceed capacity %d", n, cap);
+    return TCSE_OK;
+}
+
+int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix, int32_t n_prefix,
+                 const tcse_process_config* cfgs, int32_t n, tcse_record* out, uint64_t* trace,
+                 int32_t trace_stride, tcse_stats* stats) {
+    if (!ctx || n < 0 || n_prefix < 0 || (n > 0 && (!cfgs || !out)))
+        return fail(TCSE_EINVAL, "tcse_run_cse: bad argument");
+    if (n == 0)
+        return TCSE_OK;
+    for (int b = 0; b < n; ++b) {
+        if (cfgs[b].strategy < 0 || cfgs[b].strategy >= TCSE_STRATEGY_COUNT)
+            return fail(TCSE_EINVAL, "select_pair: unknown strategy");
+        if (cfgs[b].strategy == TCSE_MIXED) {
+            int rc = validate_mix(cfgs[b].mix_weights);
+            if (rc)
+                return rc;
+        }
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    CU(cudaSetDevice(ctx->device));
+    DevSys d;
+    HostSys probe;
+    int rc = validate_system(sys, &probe);
+    if (rc)
+        return rc;
+    const int W = launch_words(probe.w_need);
+    rc = prepare(ctx, sys, W, &d);
+    if (rc)
+        return rc;
+    rc = base_candidates(ctx, d);
+    if (rc)
+        return rc;
+    DBuf dpre, dcfg, dcost, dlen, down, dstrat, dseed, dsubs, dtrace;
+    rc = upload_pairs(ctx, prefix, n_prefix, &dpre);
+    if (rc)
+        return rc;
+    const int sub_cap = d.h.naive + 1;
+    CU(dcfg.reserve(sizeof(tcse_process_config) * size_t(n)));
+    CU(cudaMemcpyAsync(dcfg.p, cfgs, sizeof(tcse_process_config) * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    CU(dcost.reserve(4 * size_t(n)));
+    CU(dlen.reserve(4 * size_t(n)));
+    CU(down.reserve(4 * size_t(n)));
+    CU(dstrat.reserve(4 * size_t(n)));
+    CU(dseed.reserve(8 * size_t(n)));
+    CU(dsubs.reserve(4 * size_t(n) * size_t(sub_cap)));
+    if (trace && trace_stride > 0)
+        CU(dtrace.reserve(8 * size_t(n) * size_t(trace_stride)));
+    CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
+
+    LaunchDesc L;
+    std::memset(&L, 0, sizeof L);
+    L.nsys = 1;
+    L.total_blocks = n;
+    SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
+    sd.mode = kModeRun;
+    sd.base_keys = d.keys.as<u32>();
+    sd.base_cnts = d.cnts.as<u16>();
+    sd.base_m = d.base_m;
+    sd.n_local = n;
+    sd.cfgs = dcfg.as<tcse_process_config>();
+    sd.prefix = dpre.as<u32>();
+    sd.prefix_len = n_prefix;
+    sd.out_cost = dcost.as<int32_t>();
+    sd.out_len = dlen.as<int32_t>();
+    sd.out_own = down.as<int32_t>();
+    sd.out_strategy = dstrat.as<int32_t>();
+    sd.out_seed = dseed.as<u64>();
+    sd.out_subs = dsubs.as<u32>();
+    sd.trace = (trace && trace_stride > 0) ? dtrace.as<u64>() : nullptr;
+    sd.trace_stride = trace_stride;
+    L.sys[0] = sd;
+    std::vector<DevSys*> v{&d};
+    CU(cudaEventRecord(ctx->ev0, ctx->stream));
+    CU(launch_search(L, W, pick_nt(ctx, W), smem_for(ctx, W, v), ctx->stream));
+    CU(cudaEventRecord(ctx->ev1, ctx->stream));
+    rc = check_err(ctx);
+    if (rc)
+        return rc;
+    const size_t nn = size_t(n);
+    std::vector<int32_t> hcost(nn), hlen(nn), hown(nn), hstrat(nn);
+    std::vector<u64> hseed((size_t)n);
+    std::vector<u32> hsubs(size_t(n) * size_t(sub_cap));
+    CU(cudaMemcpyAsync(hcost.data(), dcost.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hlen.data(), dlen.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hown.data(), down.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hstrat.data(), dstrat.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hseed.data(), dseed.p, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hsubs.data(), dsubs.p, 4 * size_t(n) * size_t(sub_cap), cudaMemcpyDeviceToHost, ctx->stream));
+    if (sd.trace)
+        CU(cudaMemcpyAsync(trace, dtrace.p, 8 * size_t(n) * size_t(trace_stride), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    uint64_t steps = 0;
+    for (int b = 0; b < n; ++b) {
+        tcse_record& r = out[b];
+        if (hlen[size_t(b)] > r.cap)
+            return fail(TCSE_ECAPACITY, "run_cse: record %d needs %d entries, capacity %d", b, hlen[size_t(b)], r.cap);
+        for (int t = 0; t < hlen[size_t(b)]; ++t)
+            r.subs[t] = key_pair(hsubs[size_t(b) * size_t(sub_cap) + size_t(t)]);
+        r.n_subs = hlen[size_t(b)];
+        r.cost = hcost[size_t(b)];
+        r.strategy = hstrat[size_t(b)];
+        r.seed = hseed[size_t(b)];
+        steps += uint64_t(hown[size_t(b)]);
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        stats->kernel_ms = ms;
+        stats->steps = steps;
+        stats->processes = uint64_t(n);
+        stats->launches = 1;
+        stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return TCSE_OK;
+}
+
+int tcse_optimize_systems(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
+                          const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb,
+                          void* user, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
+    if (!ctx || n_systems < 1 || n_systems > kMaxSys || !systems || !best)
+        return fail(TCSE_EINVAL, "tcse_optimize_systems: bad argument (1..%d systems)", kMaxSys);
+    int rc = validate_config(cfg);
+    if (rc)
+        return rc;
+    if ((cfg->forced_strategy == TCSE_MIXED || (cfg->forced_strategy < 0 && cfg->strategy_weights[TCSE_MIXED] > 0.0)) &&
+        (rc = validate_mix(cfg->mix_weights)))
+        return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    CU(cudaSetDevice(ctx->device));
+    const int n = cfg->n_processes > 0 ? cfg->n_processes : 256;  // parallel_search.hpp:224
+    const int world = ctx->world, rank = ctx->rank;
+    // contiguous partition of global process ids
+    auto part = [&](int r) { return int((long long)n * r / world); };
+    const int p0 = part(rank), p1 = part(rank + 1), n_local = p1 - p0;
+
+    // ---- prepare systems (one launch word count for all: the max)
+    std::vector<DevSys> dev((size_t)n_systems);
+    int Wmax = 1;
+    for (int s = 0; s < n_systems; ++s) {
+        HostSys probe;
+        rc = validate_system(&systems[s], &probe);
+        if (rc)
+            return rc;
+        Wmax = std::max(Wmax, launch_words(probe.w_need));
+    }
+    const int nt = pick_nt(ctx, Wmax);
+    for (int s = 0; s < n_systems; ++s) {
+        rc = prepare(ctx, &systems[s], Wmax, &dev[size_t(s)]);
+        if (rc)
+            return rc;
+        rc = base_candidates(ctx, dev[size_t(s)]);
+        if (rc)
+            return rc;
+        if (best[s].cap < dev[size_t(s)].h.naive)
+            return fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < naive cost %d", best[s].cap,
+                        dev[size_t(s)].h.naive);
+    }
+    std::vector<DevSys*> dptr;
+    for (auto& d : dev)
+        dptr.push_back(&d);
+    const int smem = smem_for(ctx, Wmax, dptr);
+    if (smem > 227 * 1024 - 1024)
+        return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", smem);
+
+    // ---- per-system device pools
+    struct Pool {
+        DBuf cost, len, own, strat, seed, subs, reinit, inc, inc_keys, gcost, stage;
+        int sub_cap = 0;
+    };
+    std::vector<Pool> pool((size_t)n_systems);
+    int hist_n = 1;
+    for (int s = 0; s < n_systems; ++s) {
+        Pool& P = pool[size_t(s)];
+        const DevSys& d = dev[size_t(s)];
+        P.sub_cap = d.h.naive + 1;
+        const size_t nl = size_t(std::max(n_local, 1));
+        CU(P.cost.reserve(4 * nl));
+        CU(P.len.reserve(4 * nl));
+        CU(P.own.reserve(4 * nl));
+        CU(P.strat.reserve(4 * nl));
+        CU(P.seed.reserve(8 * nl));
+        CU(P.subs.reserve(4 * nl * size_t(P.sub_cap)));
+        CU(P.reinit.reserve(size_t(n)));
+        CU(P.inc.reserve(sizeof(IncState)));
+        CU(P.inc_keys.reserve(4 * size_t(P.sub_cap)));
+        CU(cudaMemsetAsync(P.inc.p, 0, sizeof(IncState), ctx->stream));
+        CU(cudaMemsetAsync(P.reinit.p, 0, size_t(n), ctx->stream));
+        if (world > 1) {
+            CU(P.gcost.reserve(4 * size_t(n)));
+            CU(P.stage.reserve(4 * size_t(P.sub_cap) + 64));
+        }
+        hist_n = std::max(hist_n, d.h.naive + 1);
+    }
+    CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
+
+    double weight_total = 0.0;
+    for (int k = 0; k < 7; ++k)
+        weight_total += cfg->strategy_weights[k];
+
+    std::vector<int> active(size_t(n_systems), 1), unchanged(size_t(n_systems), 0), iters(size_t(n_systems), 0);
+    std::vector<IncState> hinc((size_t)n_systems);
+    std::vector<std::vector<u32>> hinc_keys((size_t)n_systems);
+    std::vector<std::vector<tcse_pair>> hinc_pairs((size_t)n_systems);
+    uint64_t launches = 0, processes = 0;
+    double kernel_ms = 0.0, exchange_ms = 0.0;
+    int iteration = 0;
+    for (;;) {
+        ++iteration;
+        // ---- K1: every process of every active system
+        LaunchDesc L;
+        std::memset(&L, 0, sizeof L);
+        std::vector<int> act;
+        for (int s = 0; s < n_systems; ++s)
+            if (active[size_t(s)])
+                act.push_back(s);
+        if (act.empty())
+            break;
+        int blocks = 0;
+        for (int s : act) {
+            const DevSys& d = dev[size_t(s)];
+            Pool& P = pool[size_t(s)];
+            SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
+            sd.mode = kModeSearch;
+            sd.base_keys = d.keys.as<u32>();
+            sd.base_cnts = d.cnts.as<u16>();
+            sd.base_m = d.base_m;
+            sd.n_local = n_local;
+            sd.p0 = p0;
+            sd.block_begin = blocks;
+            sd.master_seed = cfg->master_seed;
+            sd.salt = salts ? salts[s] : uint64_t(s);
+            sd.iteration = iteration;
+            sd.forced = cfg->forced_strategy;
+            for (int k = 0; k < 7; ++k)
+                sd.weights[k] = cfg->strategy_weights[k];
+            sd.weight_total = weight_total;
+            for (int k = 0; k < 4; ++k)
+                sd.mix[k] = cfg->mix_weights[k];
+            sd.reinit = iteration >= 2 ? P.reinit.as<u8>() + p0 : nullptr;
+            sd.inc_keys = P.inc_keys.as<u32>();
+            sd.inc_len = hinc[size_t(s)].len;
+            sd.out_cost = P.cost.as<int32_t>();
+            sd.out_len = P.len.as<int32_t>();
+            sd.out_own = P.own.as<int32_t>();
+            sd.out_strategy = P.strat.as<int32_t>();
+            sd.out_seed = P.seed.as<u64>();
+            sd.out_subs = P.subs.as<u32>();
+            L.sys[L.nsys++] = sd;
+            blocks += n_local;
+        }
+        L.total_blocks = blocks;
+        if (blocks > 0) {
+            CU(cudaEventRecord(ctx->ev0, ctx->stream));
+            CU(launch_search(L, Wmax, nt, smem, ctx->stream));
+            CU(cudaEventRecord(ctx->ev1, ctx->stream));
+            ++launches;
+            processes += uint64_t(blocks);
+        }
+        const auto tx = std::chrono::steady_clock::now();
+        // ---- exchange (world > 1): costs + each rank's best record
+        ReduceLaunch RL;
+        std::memset(&RL, 0, sizeof RL);
+        for (int s : act) {
+            Pool& P = pool[size_t(s)];
+            ReduceDesc R;
+            std::memset(&R, 0, sizeof R);
+            R.n = n;
+            R.costs = P.cost.as<int32_t>();
+            R.rec_base = 0;
+            R.rec_n = n;
+            R.lens = P.len.as<int32_t>();
+            R.strategies = P.strat.as<int32_t>();
+            R.seeds = P.seed.as<u64>();
+            R.subs = P.subs.as<u32>();
+            R.stride = P.sub_cap;
+            R.own = P.own.as<int32_t>();
+            R.own_n = n_local;
+            R.inc = P.inc.as<IncState>();
+            R.inc_keys = P.inc_keys.as<u32>();
+            R.reinit_next = P.reinit.as<u8>();
+            R.fraction = cfg->reinit_fraction;
+            R.hist_n = hist_n;
+            if (world > 1) {
+                // payload per rank: n_max costs, then the local best record
+                const int n_max = (n + world - 1) / world + 1;
+                const int words = n_max + 6 + P.sub_cap;
+                std::vector<int32_t> send(size_t(words), 0), recv(size_t(words) * size_t(world), 0);
+                std::vector<int32_t> c(size_t(std::max(n_local, 1)));
+                CU(cudaMemcpyAsync(c.data(), P.cost.p, 4 * size_t(n_local), cudaMemcpyDeviceToHost, ctx->stream));
+                CU(cudaStreamSynchronize(ctx->stream));
+                rc = check_err(ctx);
+                if (rc)
+                    return rc;
+                int lb = -1;
+                for (int t = 0; t < n_local; ++t) {
+                    send[size_t(t)] = c[size_t(t)];
+                    if (lb < 0 || c[size_t(t)] < c[size_t(lb)])
+                        lb = t;
+                }
+                int32_t* hdr = send.data() + n_max;
+                hdr[0] = lb >= 0 ? 1 : 0;
+                if (lb >= 0) {
+                    int32_t len = 0, st = 0;
+                    u64 sd64 = 0;
+                    CU(cudaMemcpyAsync(&len, P.len.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                    CU(cudaMemcpyAsync(&st, P.strat.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+                    CU(cudaMemcpyAsync(&sd64, P.seed.as<u64>() + lb, 8, cudaMemcpyDeviceToHost, ctx->stream));
+                    CU(cudaStreamSynchronize(ctx->stream));
+                    hdr[1] = p0 + lb;
+                    hdr[2] = len;
+                    hdr[3] = st;
+                    std::memcpy(&hdr[4], &sd64, 8);
+                    CU(cudaMemcpyAsync(hdr + 6, P.subs.as<u32>() + size_t(lb) * size_t(P.sub_cap), 4 * size_t(len),
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+                    CU(cudaStreamSynchronize(ctx->stream));
+                }
+                if (ctx->allgather(send.data(), recv.data(), send.size() * 4, ctx->ag_user) != 0)
+                    return fail(TCSE_ENCCL, "exchange: allgather failed");
+                std::vector<int32_t> gcost((size_t)n);
+                int best_r = -1, best_p = -1, best_c = 0;
+                for (int r = 0; r < world; ++r) {
+                    const int32_t* rr = recv.data() + size_t(r) * size_t(words);
+                    for (int t = 0; t < part(r + 1) - part(r); ++t)
+                        gcost[size_t(part(r) + t)] = rr[t];
+                    const int32_t* h = rr + n_max;
+                    if (h[0] && (best_r < 0 || h[1 + 0] >= 0)) {
+                        const int bp = h[1], bc = rr[bp - part(r)];
+                        if (best_r < 0 || bc < best_c || (bc == best_c && bp < best_p)) {
+                            best_r = r;
+                            best_p = bp;
+                            best_c = bc;
+                        }
+                    }
+                }
+                const int32_t* h = recv.data() + size_t(best_r) * size_t(words) + n_max;
+                // stage: [len, strategy, seed(2 words)] + keys
+                std::vector<int32_t> stage(size_t(4 + P.sub_cap), 0);
+                stage[0] = h[2];
+                stage[1] = h[3];
+                stage[2] = h[4];
+                stage[3] = h[5];
+                std::memcpy(stage.data() + 4, h + 6, 4 * size_t(h[2]));
+                CU(cudaMemcpyAsync(P.gcost.p, gcost.data(), 4 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+                CU(cudaMemcpyAsync(P.stage.p, stage.data(), 4 * stage.size(), cudaMemcpyHostToDevice, ctx->stream));
+                R.costs = P.gcost.as<int32_t>();
+                R.rec_base = best_p;
+                R.rec_n = 1;
+                R.lens = P.stage.as<int32_t>();
+                R.strategies = P.stage.as<int32_t>() + 1;
+                R.seeds = reinterpret_cast<const u64*>(P.stage.as<int32_t>() + 2);
+                R.subs = P.stage.as<u32>() + 4;
+            }
+            RL.r[RL.nsys++] = R;
+        }
+        CU(launch_reduce(RL, hist_n, ctx->stream));
+        // ---- host: incumbent bookkeeping (patience, callback)
+        std::vector<IncState> st(act.size());
+        for (size_t a = 0; a < act.size(); ++a)
+            CU(cudaMemcpyAsync(&st[a], pool[size_t(act[a])].inc.p, sizeof(IncState), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        exchange_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx).count();
+        rc = check_err(ctx);
+        if (rc)
+            return rc;
+        if (blocks > 0) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+            kernel_ms += ms;
+        }
+        bool stop_all = false;
+        for (size_t a = 0; a < act.size(); ++a) {
+            const int s = act[a];
+            hinc[size_t(s)] = st[a];
+            iters[size_t(s)] = iteration;
+            if (st[a].improved) {
+                unchanged[size_t(s)] = 0;
+                hinc_keys[size_t(s)].resize(size_t(std::max(st[a].len, 1)));
+                if (cb) {
+                    CU(cudaMemcpyAsync(hinc_keys[size_t(s)].data(), pool[size_t(s)].inc_keys.p, 4 * size_t(st[a].len),
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+                    CU(cudaStreamSynchronize(ctx->stream));
+                }
+            } else {
+                ++unchanged[size_t(s)];
+            }
+            if (cb) {
+                auto& pairs = hinc_pairs[size_t(s)];
+                if (st[a].improved || pairs.empty()) {
+                    pairs.resize(size_t(std::max(st[a].len, 1)));
+                    for (int t = 0; t < st[a].len; ++t)
+                        pairs[size_t(t)] = key_pair(hinc_keys[size_t(s)][size_t(t)]);
+                }
+                tcse_record r;
+                r.subs = pairs.data();
+                r.cap = st[a].len;
+                r.n_subs = st[a].len;
+                r.cost = st[a].cost;
+                r.strategy = st[a].strategy;
+                r.seed = st[a].seed;
+                if (cb(s, iteration, &r, user) != 0)
+                    stop_all = true;
+            }
+            if (unchanged[size_t(s)] >= cfg->patience ||
+                (cfg->max_iterations > 0 && iteration >= cfg->max_iterations))
+                active[size_t(s)] = 0;
+        }
+        if (stop_all)
+            break;
+    }
+    // ---- results
+    uint64_t steps = 0;
+    for (int s = 0; s < n_systems; ++s) {
+        const IncState& I = hinc[size_t(s)];
+        if (I.len > best[s].cap)
+            return fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < %d", best[s].cap, I.len);
+        std::vector<u32> k(size_t(std::max(I.len, 1)));
+        CU(cudaMemcpyAsync(k.data(), pool[size_t(s)].inc_keys.p, 4 * size_t(I.len), cudaMemcpyDeviceToHost, ctx->stream));
+        IncState fin;
+        CU(cudaMemcpyAsync(&fin, pool[size_t(s)].inc.p, sizeof fin, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (int t = 0; t < I.len; ++t)
+            best[s].subs[t] = key_pair(k[size_t(t)]);
+        best[s].n_subs = I.len;
+        best[s].cost = I.cost;
+        best[s].strategy = I.strategy;
+        best[s].seed = I.seed;
+        if (iterations)
+            iterations[s] = iters[size_t(s)];
+        steps += fin.steps;
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->steps = steps;
+        stats->processes = processes;
+        stats->launches = launches;
+        stats->iterations = iteration;
+        stats->kernel_ms = kernel_ms;
+        stats->exchange_ms = exchange_ms;
+        stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return TCSE_OK;
+}
+
+int tcse_optimize_system(tcse_ctx* ctx, const tcse_system* sys, const tcse_search_config* cfg, uint64_t stream_salt,
+                         tcse_iter_cb cb, void* user, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
+    return tcse_optimize_systems(ctx, 1, sys, cfg, &stream_salt, cb, user, best, iterations, stats);
+}
+
+// replay_prefix + total_cost + expand_and_verify (linear_system.hpp:193-258)
+int tcse_verify_record(const tcse_system* sys, const tcse_pair* subs, int32_t n_subs, int32_t* cost_out) {
+    HostSys h;
+    int rc = validate_system(sys, &h);
+    if (rc && rc != TCSE_ECAPACITY)
+        return rc;
+    const int nx = sys->n_x;
+    // rows as dense signed coefficient maps over current variables
+    std::vector<std::vector<int>> rows = h.rows;
+    std::vector<tcse_pair> defs;
+    for (int t = 0; t < n_subs; ++t) {
+        const tcse_pair q = subs[t];
+        const int k = nx + int(defs.size()) + 1;
+        const int first = q.i, second = q.rel_sign * q.j;
+        int replaced = 0;
+        if (q.i >= 1 && q.j > q.i && q.j < k && (q.rel_sign == 1 || q.rel_sign == -1)) {
+            for (auto& row : rows) {
+                auto has = [&](int x) { return std::find(row.begin(), row.end(), x) != row.end(); };
+                auto erase = [&](int x) { row.erase(std::find(row.begin(), row.end(), x)); };
+                if (has(first) && has(second)) {
+                    erase(first);
+                    erase(second);
+                    row.push_back(k);
+                    ++replaced;
+                } else if (has(-first) && has(-second)) {
+                    erase(-first);
+                    erase(-second);
+                    row.push_back(-k);
+                    ++replaced;
+                }
+            }
+        }
+        if (replaced == 0)
+            return fail(TCSE_EREPLAY, "replay_prefix: unreplayable pair at position %d", t);
+        defs.push_back(q);
+    }
+    int cost = int(defs.size());
+    for (const auto& row : rows)
+        if (!row.empty())
+            cost += int(row.size()) - 1;
+    *cost_out = cost;
+    // expansion over base variables
+    std::vector<std::vector<long long>> ex(size_t(nx) + defs.size() + 1, std::vector<long long>(size_t(nx) + 1, 0));
+    for (int v = 1; v <= nx; ++v)
+        ex[size_t(v)][size_t(v)] = 1;
+    for (size_t t = 0; t < defs.size(); ++t) {
+        const size_t id = size_t(nx) + t + 1;
+        for (int b = 1; b <= nx; ++b)
+            ex[id][size_t(b)] = ex[size_t(defs[t].i)][size_t(b)] + defs[t].rel_sign * ex[size_t(defs[t].j)][size_t(b)];
+    }
+    for (int r = 0; r < sys->n_e; ++r) {
+        std::vector<long long> acc(size_t(nx) + 1, 0);
+        for (int term : rows[size_t(r)])
+            for (int b = 1; b <= nx; ++b)
+                acc[size_t(b)] += (term > 0 ? 1 : -1) * ex[size_t(std::abs(term))][size_t(b)];
+        int nonzero = 0;
+        for (int b = 1; b <= nx; ++b) {
+            if (acc[size_t(b)] == 0)
+                continue;
+            ++nonzero;
+            if (acc[size_t(b)] != 1 && acc[size_t(b)] != -1)
+                return 0;
+            const int want = acc[size_t(b)] > 0 ? b : -b;
+            if (std::find(h.rows[size_t(r)].begin(), h.rows[size_t(r)].end(), want) == h.rows[size_t(r)].end())
+                return 0;
+        }
+        if (nonzero != int(h.rows[size_t(r)].size()))
+            return 0;
+    }
+    return 1;
+}
+
+}  // extern "C"
