@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py — CSE substitution steps/s of the B200 search path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2]): the 4x4x4 rank-49 Strassen(x)Strassen
+scheme (tests/golden/schemes/sxs.json, digest 7da4ac65bf44d830), reference
+default mixed strategy weights {ga 4, wr 1, gr 2, gi 8, mix 0.1, gp 0.01},
+reinit fraction 0.4 (best-pool sharing), N = 16384 processes per component
+(the paper's GPU process count for rank < 100), master seed
+1, the U, V and W expression sets optimized concurrently.  A STEP is one
+optimize_system iteration (parallel_search.hpp:231-271) of all three
+components: N processes each run to completion, then the iteration barrier
+(incumbent pool update + reinit selection).  Patience is set high so every
+timed step is a full iteration (results are bit-identical to the reference
+for the same iterations).  The metric counts substitutions selected by
+run_cse (cse_engine.hpp:33-40); replayed prefixes are excluded.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Multi-GPU: torchrun, one rank per GPU; processes are partitioned by global id
+(weak: each rank runs N processes per component, total N*world), and the
+per-iteration exchange (costs + best record all-gather) keeps the search
+identical to a single-process run of N*world processes.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "CSE substitution steps/sec (1/2/4/8 B200) & best additions at fixed wall-time"
+WORKLOAD = "sxs"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tcse", choices=["tcse", "reference"])
+    ap.add_argument("--workload", default=WORKLOAD)
+    ap.add_argument("--processes", type=int, default=16384)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_systems(name):
+    import paper_2512_13365_b200 as T
+    s = T.load_scheme(os.path.join(ROOT, "tests", "golden", "schemes", name + ".json"))
+    return s, T.extract_systems(s)
+
+
+def config_block(args, world, scaling="weak"):
+    s, _ = load_systems(args.workload)
+    return {
+        "workload": "%s %dx%dx%d:%d, mixed strategies (reference default weights), reinit 0.4, "
+                    "%d processes/component/GPU, U/V/W concurrent; step = one optimize_system iteration"
+                    % (args.workload, s["m"], s["n"], s["p"], s["r"], args.processes),
+        "scheme_digest": "7da4ac65bf44d830" if args.workload == "sxs" else None,
+        "processes_per_gpu": args.processes,
+        "processes_total": args.processes * world,
+        "master_seed": args.seed,
+        "parallelism": "process-partition x%d (per-iteration all-gather exchange)" % world,
+        "l2": "flushed before every timed step (256 MiB write)",
+    }
+
+
+# --------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    """The reference's own optimize_system (oracle/_ref, compiled from the
+    unmodified headers) on the host cores, same workload, same iterations."""
+    if rank != 0:
+        return 0
+    from oracle_lib import reference
+    import paper_2512_13365_b200 as T
+    from paper_2512_13365_b200 import _abi
+    ref = reference()
+    ref.ref_optimize_system_timed.argtypes = [
+        C.POINTER(_abi.System), C.POINTER(_abi.SearchConfig), C.c_uint64, C.c_uint32, C.c_double,
+        C.POINTER(_abi.Record), C.POINTER(C.c_int32), C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+        C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]
+    threads = os.cpu_count() or 1
+    _, systems = load_systems(args.workload)
+    n_proc = args.processes * args.gpus  # the same global process count as the GPU arm
+    its = args.warmup + args.steps
+    cfg = T.SearchConfig(n_processes=n_proc, patience=1 << 30, master_seed=args.seed, max_iterations=its).to_c()
+    secs = steps = 0.0
+    for comp, (nx, rows) in enumerate(systems):
+        s = _abi.make_system(nx, rows)
+        rec = _abi.make_record(T.naive_cost(rows) + 1)
+        it, st, tot = C.c_int32(), C.c_uint64(), C.c_double()
+        isecs = (C.c_double * its)()
+        isteps = (C.c_uint64 * its)()
+        rc = ref.ref_optimize_system_timed(C.byref(s), C.byref(cfg), comp, threads, 0.0, C.byref(rec), C.byref(it),
+                                           C.byref(st), C.byref(tot), isecs, isteps, its)
+        if rc:
+            raise RuntimeError(ref.ref_last_error().decode())
+        secs += sum(isecs[args.warmup:its])
+        steps += sum(isteps[args.warmup:its])
+    value = steps / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "substitution steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic (fixed public scheme)",
+        "config": config_block(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "substitution steps/s", "cores": threads, "kind": "reference",
+                         "sample": "iterations %d..%d of optimize_system on U, V, W (sequential, as "
+                                   "optimize_scheme runs them), %d processes each, threads=%d"
+                                   % (args.warmup + 1, its, n_proc, threads)},
+        "e2e": {"value": value, "unit": "substitution steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "substitution_steps": int(steps),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline_sample(args):
+    """Bounded sample of the same workload on the reference CPU path: the
+    first optimize_system iteration of U, V and W with every host thread."""
+    from oracle_lib import reference
+    import paper_2512_13365_b200 as T
+    from paper_2512_13365_b200 import _abi
+    ref = reference()
+    threads = os.cpu_count() or 1
+    _, systems = load_systems(args.workload)
+    cfg = T.SearchConfig(n_processes=args.processes, patience=1 << 30, master_seed=args.seed,
+                         max_iterations=1).to_c()
+    secs = steps = 0.0
+    for comp, (nx, rows) in enumerate(systems):
+        s = _abi.make_system(nx, rows)
+        rec = _abi.make_record(T.naive_cost(rows) + 1)
+        it, st, tot = C.c_int32(), C.c_uint64(), C.c_double()
+        rc = ref.ref_optimize_system_counted(C.byref(s), C.byref(cfg), comp, threads, 0.0, C.byref(rec),
+                                             C.byref(it), C.byref(st), C.byref(tot))
+        if rc:
+            raise RuntimeError(ref.ref_last_error().decode())
+        secs += tot.value
+        steps += st.value
+    return {"value": steps / secs, "unit": "substitution steps/s", "cores": threads, "kind": "reference",
+            "sample": "iteration 1 of optimize_system on U, V, W (%d processes each, %.0f steps, %.1f s), "
+                      "threads=%d, oracle/_ref built from the reference headers with its Release flags"
+                      % (args.processes, steps, secs, threads)}
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2512_13365_b200 as T
+
+    torch.cuda.set_device(local)
+    gloo = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        gloo = dist.new_group(backend="gloo")
+
+    def allgather(data):
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=gloo)
+        return [o.numpy().tobytes() for o in out]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    dev = T.Device(local)
+    dev.set_partition(rank, world, allgather if world > 1 else None)
+    stream = torch.cuda.current_stream()
+    dev.set_stream(stream.cuda_stream)
+    _, sys_rows = load_systems(args.workload)
+    systems = [T.LinearSystem(nx, rows) for nx, rows in sys_rows]
+    n_total = args.processes * world
+    cfg = T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    search = T.Search(systems, cfg, [0, 1, 2], device=dev)
+    for _ in range(args.warmup):
+        search.step()
+    torch.cuda.synchronize()
+    s0 = search.stats()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    total_ms = 0.0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        search.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+    s1 = search.stats()
+    steps_local = s1["steps"] - s0["steps"]
+    kernel_ms = s1["kernel_ms"] - s0["kernel_ms"]
+    wops = s1["wops"] - s0["wops"]
+    launches = s1["launches"] - s0["launches"]
+    results, _ = search.result()
+    search.close()
+
+    # ---- e2e: the public call (host CSR in, host records out), K iterations
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        torch.cuda.synchronize()
+        st = {}
+        t0 = time.perf_counter()
+        T.optimize_systems(systems, T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed,
+                                                   max_iterations=args.steps), [0, 1, 2], device=dev, stats=st)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e = {"steps": st["steps"], "secs": e2e_s, "h2d": st["h2d_bytes"], "d2h": st["d2h_bytes"]}
+    clk = clocks.stop()
+    peak_gops = dev.microbench_wordops()
+
+    # ---- cross-rank aggregation (max time, summed work)
+    vals = torch.tensor([total_ms, float(steps_local), float(wops), kernel_ms,
+                         e2e["secs"] if e2e else 0.0, float(e2e["steps"] if e2e else 0)], dtype=torch.float64)
+    if world > 1:
+        mx = vals.clone().cuda()
+        sm = vals.clone().cuda()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        mx, sm = mx.cpu(), sm.cpu()
+    else:
+        mx = sm = vals
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    t_ms = mx[0].item()
+    steps_all = sm[1].item()
+    value = steps_all / (t_ms / 1e3)
+    # roofline of the dominant kernel (search_kernel): algorithmic word-ops per
+    # launch (SURVEY.md 8(d) model, counted by the kernel) / average launch
+    # duration (CUDA events on the launch stream) vs the measured smem word-op peak
+    per_launch = wops / max(1, launches)
+    avg_launch_ms = kernel_ms / max(1, launches)
+    achieved = per_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "search_kernel_dram.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "substitution steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (fixed public scheme; search randomness from the seed only)",
+        "config": config_block(args, world),
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_gops, "unit": "Gword-ops/s",
+                     "frac": achieved / peak_gops if peak_gops else None, "traffic": traffic,
+                     "peak_source": "in-repo microbenchmark (tcse_microbench_wordops) on this GPU",
+                     "kernel": "search_kernel<W=1,NT=128>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms)},
+        "clocks": clk,
+        "gpu_launches": int(2 * args.steps),
+        "substitution_steps": int(steps_all),
+        "incumbent_costs": [r.cost for r, _ in results],
+    }
+    if e2e:
+        line["e2e"] = {"value": sm[5].item() / mx[4].item(), "unit": "substitution steps/s",
+                       "h2d_bytes_per_step": e2e["h2d"] / args.steps, "d2h_bytes_per_step": e2e["d2h"] / args.steps,
+                       "call": "tcse_optimize_systems (C ABI, host CSR in, host records out), %d iterations"
+                               % args.steps}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_sample(args)
+        except Exception as e:  # the checker must not take the bench down
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

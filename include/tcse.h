@@ -132,9 +132,13 @@ typedef struct tcse_stats {
     uint64_t launches;     /* search-kernel launches */
     int32_t iterations;    /* iteration barriers passed (max over systems) */
     int32_t reserved;
-    double kernel_ms;      /* summed search-kernel time (CUDA events) */
-    double wall_ms;        /* whole call */
-    double exchange_ms;    /* reduce + cross-rank exchange time */
+    double kernel_ms;      /* summed search-kernel time (CUDA events on the launch stream) */
+    double step_ms;        /* summed iteration time on the device: search + reduce (CUDA events) */
+    double wall_ms;        /* whole call, host clock */
+    double exchange_ms;    /* host time from search launch to incumbent state read-back */
+    uint64_t h2d_bytes;    /* host->device bytes copied by the call */
+    uint64_t d2h_bytes;    /* device->host bytes copied by the call */
+    uint64_t wops;         /* algorithmic word-intersections (SURVEY.md 8(d) model) */
 } tcse_stats;
 
 /* Called on the calling thread after every iteration barrier, like
@@ -148,6 +152,7 @@ typedef int (*tcse_iter_cb)(int32_t system_index, int32_t iteration,
 typedef int (*tcse_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
 
 typedef struct tcse_ctx tcse_ctx;
+typedef struct tcse_search tcse_search;
 
 const char* tcse_last_error(void);
 int32_t tcse_abi_version(void);
@@ -164,6 +169,11 @@ int32_t tcse_naive_cost(const tcse_system* sys);
  * partition.  NULL on failure (see tcse_last_error). */
 tcse_ctx* tcse_create(int32_t device);
 void tcse_destroy(tcse_ctx* ctx);
+
+/* Launch on a caller-owned cudaStream_t (NULL = the context's own stream),
+ * e.g. torch.cuda.current_stream().cuda_stream so that caller-side CUDA
+ * events bracket the work. */
+int tcse_set_stream(tcse_ctx* ctx, void* stream);
 
 /* Process partition across ranks: this rank runs global process ids
  * [floor(p*rank/world) ...) of every iteration; allgather exchanges the
@@ -209,6 +219,24 @@ int tcse_optimize_systems(tcse_ctx* ctx, int32_t n_systems, const tcse_system* s
                           const tcse_search_config* cfg, const uint64_t* salts,
                           tcse_iter_cb cb, void* user, tcse_record* best,
                           int32_t* iterations, tcse_stats* stats);
+
+/* The same search, advanced one iteration barrier at a time (what
+ * tcse_optimize_systems loops over): create uploads and prepares the systems,
+ * each step runs one iteration for every still-active system and reports how
+ * many remain active (0 = all converged or the callback stopped the search),
+ * result copies the incumbents out. */
+int tcse_search_create(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
+                       const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb,
+                       void* user, tcse_search** out);
+int tcse_search_step(tcse_search* search, int32_t* n_active);
+int tcse_search_result(tcse_search* search, tcse_record* best, int32_t* iterations,
+                       tcse_stats* stats);
+void tcse_search_destroy(tcse_search* search);
+
+/* Measured shared-memory word-op peak of this device (roofline
+ * denominator): a microbenchmark of the search kernel's inner operation
+ * (two 8-byte LDS, AND, POPC, accumulate) over every SM.  *gops = Gword-ops/s. */
+int tcse_microbench_wordops(tcse_ctx* ctx, double* gops);
 
 /* Host-side result/verification API kept from the reference (no GPU):
  * replay_prefix + total_cost + expand_and_verify (linear_system.hpp:193-258,

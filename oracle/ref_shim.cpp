@@ -208,9 +208,10 @@ int ref_optimize_system(const tcse_system* sys, const tcse_search_config* cfg, u
 // optimize_system re-expressed with the reference's own building blocks plus
 // a substitution-step counter and optional stop knobs (max_iterations,
 // wall_budget_s checked at the barrier like an on_iteration abort).
-int ref_optimize_system_counted(const tcse_system* sys, const tcse_search_config* c, uint64_t salt,
-                                uint32_t threads, double wall_budget_s, tcse_record* best,
-                                int32_t* iterations, uint64_t* steps, double* seconds) {
+int ref_optimize_system_timed(const tcse_system* sys, const tcse_search_config* c, uint64_t salt,
+                              uint32_t threads, double wall_budget_s, tcse_record* best,
+                              int32_t* iterations, uint64_t* steps, double* seconds,
+                              double* iter_secs, uint64_t* iter_steps, int32_t iter_cap) {
     return guarded([&]() -> int {
         const auto t0 = std::chrono::steady_clock::now();
         const LinearSystem base = to_system(sys);
@@ -222,6 +223,8 @@ int ref_optimize_system_counted(const tcse_system* sys, const tcse_search_config
         auto results = std::vector<SolutionRecord>(std::size_t(n));
         std::atomic<std::uint64_t> counted{0};
         int unchanged = 0, iteration = 0;
+        auto t_iter = std::chrono::steady_clock::now();
+        std::uint64_t steps_before = 0;
         for (;;) {
             ++iteration;
             const auto slots = assign_strategies(cfg, iteration, n, salt);
@@ -253,7 +256,14 @@ int ref_optimize_system_counted(const tcse_system* sys, const tcse_search_config
             } else {
                 ++unchanged;
             }
-            const double elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            const auto now = std::chrono::steady_clock::now();
+            const double elapsed = std::chrono::duration<double>(now - t0).count();
+            if (iter_secs && iteration - 1 < iter_cap) {
+                iter_secs[iteration - 1] = std::chrono::duration<double>(now - t_iter).count();
+                iter_steps[iteration - 1] = counted.load() - steps_before;
+            }
+            t_iter = now;
+            steps_before = counted.load();
             if (unchanged >= cfg.patience)
                 break;
             if (c->max_iterations > 0 && iteration >= c->max_iterations)
@@ -266,6 +276,13 @@ int ref_optimize_system_counted(const tcse_system* sys, const tcse_search_config
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return put_record(*incumbent, best);
     });
+}
+
+int ref_optimize_system_counted(const tcse_system* sys, const tcse_search_config* c, uint64_t salt,
+                                uint32_t threads, double wall_budget_s, tcse_record* best,
+                                int32_t* iterations, uint64_t* steps, double* seconds) {
+    return ref_optimize_system_timed(sys, c, salt, threads, wall_budget_s, best, iterations, steps, seconds,
+                                     nullptr, nullptr, 0);
 }
 
 int ref_verify_record(const tcse_system* sys, const tcse_pair* subs, int32_t n_subs, int32_t* cost_out) {

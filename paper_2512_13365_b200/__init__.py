@@ -27,7 +27,7 @@ from .scheme import (SchemeError, extract_systems, load_scheme, naive_cost, pars
 
 __all__ = [
     "TcseError", "LinearSystem", "ProcessConfig", "SearchConfig", "SolutionRecord", "Device",
-    "count_pairs", "run_cse", "optimize_system", "optimize_systems", "optimize_scheme",
+    "count_pairs", "run_cse", "optimize_system", "optimize_systems", "optimize_scheme", "Search",
     "verify_record", "report_to_json", "strategy_from_string", "library_path",
     "parse_scheme", "load_scheme", "extract_systems", "naive_cost", "scheme_digest", "verify_brent",
     "SchemeError", "STRATEGY_NAMES", "STRATEGY_SHORT", "DEFAULT_WEIGHTS",
@@ -81,6 +81,13 @@ def lib():
                                             P(C.c_uint64), _abi.ITER_CB, C.c_void_p, P(_abi.Record),
                                             P(C.c_int32), P(_abi.Stats)]
         L.tcse_verify_record.argtypes = [P(_abi.System), P(_abi.Pair), C.c_int32, P(C.c_int32)]
+        L.tcse_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+        L.tcse_microbench_wordops.argtypes = [C.c_void_p, P(C.c_double)]
+        L.tcse_search_create.argtypes = [C.c_void_p, C.c_int32, P(_abi.System), P(_abi.SearchConfig),
+                                         P(C.c_uint64), _abi.ITER_CB, C.c_void_p, P(C.c_void_p)]
+        L.tcse_search_step.argtypes = [C.c_void_p, P(C.c_int32)]
+        L.tcse_search_result.argtypes = [C.c_void_p, P(_abi.Record), P(C.c_int32), P(_abi.Stats)]
+        L.tcse_search_destroy.argtypes = [C.c_void_p]
         _lib = L
         return L
 
@@ -211,6 +218,16 @@ class Device:
             self._cb = _abi.ALLGATHER_FN(0)
         _check(lib().tcse_set_partition(self._h, rank, world, self._cb, None))
 
+    def set_stream(self, stream_ptr):
+        """Launch on a caller-owned cudaStream_t (int pointer; 0 = own stream)."""
+        _check(lib().tcse_set_stream(self._h, C.c_void_p(stream_ptr or None)))
+
+    def microbench_wordops(self):
+        """Measured shared-memory word-op peak (Gword-ops/s) of this device."""
+        g = C.c_double()
+        _check(lib().tcse_microbench_wordops(self._h, C.byref(g)))
+        return g.value
+
     @property
     def handle(self):
         return self._h
@@ -277,6 +294,73 @@ def run_cse(sys, cfgs, prefix=(), trace_stride=0, device=None, stats=None):
                   for b in range(n)]
         return out, traces
     return out
+
+
+def _stats_dict(st):
+    return {k: getattr(st, k) for k, _ in _abi.Stats._fields_}
+
+
+class Search:
+    """optimize_systems advanced one iteration barrier at a time
+    (tcse_search_create / step / result)."""
+
+    def __init__(self, systems, cfg, salts=None, on_iteration=None, device=None):
+        self.systems = [_as_system(s) for s in systems]
+        self.device = device or default_device()
+        n = len(self.systems)
+        self._sarr = (_abi.System * n)()
+        for t, s in enumerate(self.systems):
+            self._sarr[t] = s.c
+        salts = list(range(n)) if salts is None else list(salts)
+        self._salts = (C.c_uint64 * n)(*salts)
+        self._cfg = cfg.to_c() if hasattr(cfg, "to_c") else cfg
+        if on_iteration is not None:
+            def cb(sys_index, iteration, inc, user):
+                try:
+                    return 1 if on_iteration(sys_index, iteration, SolutionRecord.from_c(inc.contents)) else 0
+                except Exception:
+                    return 1
+            self._cfun = _abi.ITER_CB(cb)
+        else:
+            self._cfun = _abi.ITER_CB(0)
+        h = C.c_void_p()
+        _check(lib().tcse_search_create(self.device.handle, n, self._sarr, C.byref(self._cfg), self._salts,
+                                        self._cfun, None, C.byref(h)))
+        self._h = h
+        self.active = n
+
+    def step(self):
+        left = C.c_int32()
+        _check(lib().tcse_search_step(self._h, C.byref(left)))
+        self.active = left.value
+        return self.active
+
+    def result(self):
+        n = len(self.systems)
+        recs = [make_record(s.naive_cost() + 1) for s in self.systems]
+        rarr = (_abi.Record * n)()
+        for t in range(n):
+            rarr[t] = recs[t]
+        its = (C.c_int32 * n)()
+        st = _abi.Stats()
+        _check(lib().tcse_search_result(self._h, rarr, its, C.byref(st)))
+        return [(SolutionRecord.from_c(rarr[t]), its[t]) for t in range(n)], _stats_dict(st)
+
+    def stats(self):
+        st = _abi.Stats()
+        _check(lib().tcse_search_result(self._h, None, None, C.byref(st)))
+        return _stats_dict(st)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tcse_search_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def optimize_systems(systems, cfg, salts=None, on_iteration=None, device=None, stats=None):

@@ -87,8 +87,12 @@ class Stats(C.Structure):
         ("iterations", C.c_int32),
         ("reserved", C.c_int32),
         ("kernel_ms", C.c_double),
+        ("step_ms", C.c_double),
         ("wall_ms", C.c_double),
         ("exchange_ms", C.c_double),
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
+        ("wops", C.c_uint64),
     ]
 
 

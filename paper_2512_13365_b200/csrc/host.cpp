@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "launch.h"
@@ -44,6 +45,8 @@ struct ReduceDesc {
     const u32* subs;
     int32_t stride;
     const int32_t* own;
+    const int32_t* own_len;
+    const u64* own_wops;
     int32_t own_n;
     IncState* inc;
     u32* inc_keys;
@@ -202,6 +205,7 @@ std::vector<u64> pack_masks(const HostSys& h, int W) {
 struct tcse_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t owned_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int nt = 128;
     int rank = 0, world = 1;
@@ -260,6 +264,7 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.n_x = d.h.n_x;
     sd.n_e = d.h.n_e;
     sd.naive = d.h.naive;
+    sd.words = d.h.w_need;
     sd.vcap = d.h.vcap;
     sd.mcap = d.h.mcap;
     sd.sub_cap = d.h.naive + 1;
@@ -453,13 +458,24 @@ void tcse_destroy(tcse_ctx* ctx) {
     if (!ctx)
         return;
     cudaSetDevice(ctx->device);
-    if (ctx->stream)
+    if (ctx->owned_stream)
+        cudaStreamDestroy(ctx->owned_stream);
+    else if (ctx->stream)
         cudaStreamDestroy(ctx->stream);
     if (ctx->ev0)
         cudaEventDestroy(ctx->ev0);
     if (ctx->ev1)
         cudaEventDestroy(ctx->ev1);
     delete ctx;
+}
+
+int tcse_set_stream(tcse_ctx* ctx, void* stream) {
+    if (!ctx)
+        return fail(TCSE_EINVAL, "tcse_set_stream: null context");
+    if (ctx->owned_stream == nullptr)
+        ctx->owned_stream = ctx->stream;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->owned_stream;
+    return TCSE_OK;
 }
 
 int tcse_set_partition(tcse_ctx* ctx, int32_t rank, int32_t world, tcse_allgather_fn allgather, void* user) {
@@ -635,332 +651,487 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     return TCSE_OK;
 }
 
-int tcse_optimize_systems(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
-                          const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb,
-                          void* user, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
-    if (!ctx || n_systems < 1 || n_systems > kMaxSys || !systems || !best)
-        return fail(TCSE_EINVAL, "tcse_optimize_systems: bad argument (1..%d systems)", kMaxSys);
+}  // extern "C"
+
+// ---------------------------------------------------------------- session
+
+namespace {
+
+struct Pool {
+    DBuf cost, len, own, strat, seed, wops, subs, reinit, inc, inc_keys, gcost, stage;
+    int sub_cap = 0;
+};
+
+}  // namespace
+
+// One optimize_systems run, advanced one iteration barrier at a time.
+struct tcse_search {
+    tcse_ctx* ctx = nullptr;
+    int n_systems = 0;
+    tcse_search_config cfg;
+    std::vector<uint64_t> salts;
+    tcse_iter_cb cb = nullptr;
+    void* user = nullptr;
+    int n = 0, p0 = 0, n_local = 0, Wmax = 1, nt = 128, smem = 0, hist_n = 1;
+    double weight_total = 0.0;
+    std::unique_ptr<DevSys[]> dev;
+    std::unique_ptr<Pool[]> pool;
+    std::vector<int> active, unchanged, iters;
+    std::vector<IncState> hinc;
+    std::vector<std::vector<u32>> hinc_keys;
+    std::vector<std::vector<tcse_pair>> hinc_pairs;
+    uint64_t launches = 0, processes = 0, h2d = 0, d2h = 0;
+    double kernel_ms = 0.0, step_ms = 0.0, exchange_ms = 0.0;
+    int iteration = 0;
+    bool stopped = false;
+    cudaEvent_t es0 = nullptr, es1 = nullptr;
+    std::chrono::steady_clock::time_point t0;
+    ~tcse_search() {
+        if (es0)
+            cudaEventDestroy(es0);
+        if (es1)
+            cudaEventDestroy(es1);
+    }
+};
+
+namespace {
+
+int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
+                const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb, void* user) {
+    if (!ctx || n_systems < 1 || n_systems > kMaxSys || !systems)
+        return fail(TCSE_EINVAL, "optimize_systems: bad argument (1..%d systems)", kMaxSys);
     int rc = validate_config(cfg);
     if (rc)
         return rc;
     if ((cfg->forced_strategy == TCSE_MIXED || (cfg->forced_strategy < 0 && cfg->strategy_weights[TCSE_MIXED] > 0.0)) &&
         (rc = validate_mix(cfg->mix_weights)))
         return rc;
-    const auto t0 = std::chrono::steady_clock::now();
+    S->t0 = std::chrono::steady_clock::now();
     CU(cudaSetDevice(ctx->device));
-    const int n = cfg->n_processes > 0 ? cfg->n_processes : 256;  // parallel_search.hpp:224
+    S->ctx = ctx;
+    S->n_systems = n_systems;
+    S->cfg = *cfg;
+    S->cb = cb;
+    S->user = user;
+    for (int s = 0; s < n_systems; ++s)
+        S->salts.push_back(salts ? salts[s] : uint64_t(s));
+    S->n = cfg->n_processes > 0 ? cfg->n_processes : 256;  // parallel_search.hpp:224
     const int world = ctx->world, rank = ctx->rank;
-    // contiguous partition of global process ids
-    auto part = [&](int r) { return int((long long)n * r / world); };
-    const int p0 = part(rank), p1 = part(rank + 1), n_local = p1 - p0;
-
-    // ---- prepare systems (one launch word count for all: the max)
-    std::vector<DevSys> dev((size_t)n_systems);
-    int Wmax = 1;
+    S->p0 = int((long long)S->n * rank / world);
+    S->n_local = int((long long)S->n * (rank + 1) / world) - S->p0;
+    S->dev.reset(new DevSys[size_t(n_systems)]);
+    S->pool.reset(new Pool[size_t(n_systems)]);
     for (int s = 0; s < n_systems; ++s) {
         HostSys probe;
         rc = validate_system(&systems[s], &probe);
         if (rc)
             return rc;
-        Wmax = std::max(Wmax, launch_words(probe.w_need));
+        S->Wmax = std::max(S->Wmax, launch_words(probe.w_need));
     }
-    const int nt = pick_nt(ctx, Wmax);
-    for (int s = 0; s < n_systems; ++s) {
-        rc = prepare(ctx, &systems[s], Wmax, &dev[size_t(s)]);
-        if (rc)
-            return rc;
-        rc = base_candidates(ctx, dev[size_t(s)]);
-        if (rc)
-            return rc;
-        if (best[s].cap < dev[size_t(s)].h.naive)
-            return fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < naive cost %d", best[s].cap,
-                        dev[size_t(s)].h.naive);
-    }
+    S->nt = pick_nt(ctx, S->Wmax);
     std::vector<DevSys*> dptr;
-    for (auto& d : dev)
-        dptr.push_back(&d);
-    const int smem = smem_for(ctx, Wmax, dptr);
-    if (smem > 227 * 1024 - 1024)
-        return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", smem);
-
-    // ---- per-system device pools
-    struct Pool {
-        DBuf cost, len, own, strat, seed, subs, reinit, inc, inc_keys, gcost, stage;
-        int sub_cap = 0;
-    };
-    std::vector<Pool> pool((size_t)n_systems);
-    int hist_n = 1;
     for (int s = 0; s < n_systems; ++s) {
-        Pool& P = pool[size_t(s)];
-        const DevSys& d = dev[size_t(s)];
+        DevSys& d = S->dev[size_t(s)];
+        rc = prepare(ctx, &systems[s], S->Wmax, &d);
+        if (rc)
+            return rc;
+        S->h2d += uint64_t(d.h.n_x) * 2 * uint64_t(S->Wmax) * 8;
+        rc = base_candidates(ctx, d);
+        if (rc)
+            return rc;
+        dptr.push_back(&d);
+    }
+    S->smem = smem_for(ctx, S->Wmax, dptr);
+    if (S->smem > 227 * 1024 - 1024)
+        return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", S->smem);
+    for (int s = 0; s < n_systems; ++s) {
+        Pool& P = S->pool[size_t(s)];
+        const DevSys& d = S->dev[size_t(s)];
         P.sub_cap = d.h.naive + 1;
-        const size_t nl = size_t(std::max(n_local, 1));
+        const size_t nl = size_t(std::max(S->n_local, 1));
         CU(P.cost.reserve(4 * nl));
         CU(P.len.reserve(4 * nl));
         CU(P.own.reserve(4 * nl));
         CU(P.strat.reserve(4 * nl));
         CU(P.seed.reserve(8 * nl));
+        CU(P.wops.reserve(8 * nl));
         CU(P.subs.reserve(4 * nl * size_t(P.sub_cap)));
-        CU(P.reinit.reserve(size_t(n)));
+        CU(P.reinit.reserve(size_t(S->n)));
         CU(P.inc.reserve(sizeof(IncState)));
         CU(P.inc_keys.reserve(4 * size_t(P.sub_cap)));
         CU(cudaMemsetAsync(P.inc.p, 0, sizeof(IncState), ctx->stream));
-        CU(cudaMemsetAsync(P.reinit.p, 0, size_t(n), ctx->stream));
+        CU(cudaMemsetAsync(P.reinit.p, 0, size_t(S->n), ctx->stream));
         if (world > 1) {
-            CU(P.gcost.reserve(4 * size_t(n)));
+            CU(P.gcost.reserve(4 * size_t(S->n)));
             CU(P.stage.reserve(4 * size_t(P.sub_cap) + 64));
         }
-        hist_n = std::max(hist_n, d.h.naive + 1);
+        S->hist_n = std::max(S->hist_n, d.h.naive + 1);
     }
     CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
-
-    double weight_total = 0.0;
     for (int k = 0; k < 7; ++k)
-        weight_total += cfg->strategy_weights[k];
+        S->weight_total += cfg->strategy_weights[k];
+    S->active.assign(size_t(n_systems), 1);
+    S->unchanged.assign(size_t(n_systems), 0);
+    S->iters.assign(size_t(n_systems), 0);
+    S->hinc.assign(size_t(n_systems), IncState());
+    std::memset(S->hinc.data(), 0, sizeof(IncState) * size_t(n_systems));
+    S->hinc_keys.assign(size_t(n_systems), {});
+    S->hinc_pairs.assign(size_t(n_systems), {});
+    CU(cudaEventCreate(&S->es0));
+    CU(cudaEventCreate(&S->es1));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return TCSE_OK;
+}
 
-    std::vector<int> active(size_t(n_systems), 1), unchanged(size_t(n_systems), 0), iters(size_t(n_systems), 0);
-    std::vector<IncState> hinc((size_t)n_systems);
-    std::vector<std::vector<u32>> hinc_keys((size_t)n_systems);
-    std::vector<std::vector<tcse_pair>> hinc_pairs((size_t)n_systems);
-    uint64_t launches = 0, processes = 0;
-    double kernel_ms = 0.0, exchange_ms = 0.0;
-    int iteration = 0;
-    for (;;) {
-        ++iteration;
-        // ---- K1: every process of every active system
-        LaunchDesc L;
-        std::memset(&L, 0, sizeof L);
-        std::vector<int> act;
-        for (int s = 0; s < n_systems; ++s)
-            if (active[size_t(s)])
-                act.push_back(s);
-        if (act.empty())
-            break;
-        int blocks = 0;
-        for (int s : act) {
-            const DevSys& d = dev[size_t(s)];
-            Pool& P = pool[size_t(s)];
-            SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
-            sd.mode = kModeSearch;
-            sd.base_keys = d.keys.as<u32>();
-            sd.base_cnts = d.cnts.as<u16>();
-            sd.base_m = d.base_m;
-            sd.n_local = n_local;
-            sd.p0 = p0;
-            sd.block_begin = blocks;
-            sd.master_seed = cfg->master_seed;
-            sd.salt = salts ? salts[s] : uint64_t(s);
-            sd.iteration = iteration;
-            sd.forced = cfg->forced_strategy;
-            for (int k = 0; k < 7; ++k)
-                sd.weights[k] = cfg->strategy_weights[k];
-            sd.weight_total = weight_total;
-            for (int k = 0; k < 4; ++k)
-                sd.mix[k] = cfg->mix_weights[k];
-            sd.reinit = iteration >= 2 ? P.reinit.as<u8>() + p0 : nullptr;
-            sd.inc_keys = P.inc_keys.as<u32>();
-            sd.inc_len = hinc[size_t(s)].len;
-            sd.out_cost = P.cost.as<int32_t>();
-            sd.out_len = P.len.as<int32_t>();
-            sd.out_own = P.own.as<int32_t>();
-            sd.out_strategy = P.strat.as<int32_t>();
-            sd.out_seed = P.seed.as<u64>();
-            sd.out_subs = P.subs.as<u32>();
-            L.sys[L.nsys++] = sd;
-            blocks += n_local;
-        }
-        L.total_blocks = blocks;
-        if (blocks > 0) {
-            CU(cudaEventRecord(ctx->ev0, ctx->stream));
-            CU(launch_search(L, Wmax, nt, smem, ctx->stream));
-            CU(cudaEventRecord(ctx->ev1, ctx->stream));
-            ++launches;
-            processes += uint64_t(blocks);
-        }
-        const auto tx = std::chrono::steady_clock::now();
-        // ---- exchange (world > 1): costs + each rank's best record
-        ReduceLaunch RL;
-        std::memset(&RL, 0, sizeof RL);
-        for (int s : act) {
-            Pool& P = pool[size_t(s)];
-            ReduceDesc R;
-            std::memset(&R, 0, sizeof R);
-            R.n = n;
-            R.costs = P.cost.as<int32_t>();
-            R.rec_base = 0;
-            R.rec_n = n;
-            R.lens = P.len.as<int32_t>();
-            R.strategies = P.strat.as<int32_t>();
-            R.seeds = P.seed.as<u64>();
-            R.subs = P.subs.as<u32>();
-            R.stride = P.sub_cap;
-            R.own = P.own.as<int32_t>();
-            R.own_n = n_local;
-            R.inc = P.inc.as<IncState>();
-            R.inc_keys = P.inc_keys.as<u32>();
-            R.reinit_next = P.reinit.as<u8>();
-            R.fraction = cfg->reinit_fraction;
-            R.hist_n = hist_n;
-            if (world > 1) {
-                // payload per rank: n_max costs, then the local best record
-                const int n_max = (n + world - 1) / world + 1;
-                const int words = n_max + 6 + P.sub_cap;
-                std::vector<int32_t> send(size_t(words), 0), recv(size_t(words) * size_t(world), 0);
-                std::vector<int32_t> c(size_t(std::max(n_local, 1)));
-                CU(cudaMemcpyAsync(c.data(), P.cost.p, 4 * size_t(n_local), cudaMemcpyDeviceToHost, ctx->stream));
-                CU(cudaStreamSynchronize(ctx->stream));
-                rc = check_err(ctx);
-                if (rc)
-                    return rc;
-                int lb = -1;
-                for (int t = 0; t < n_local; ++t) {
-                    send[size_t(t)] = c[size_t(t)];
-                    if (lb < 0 || c[size_t(t)] < c[size_t(lb)])
-                        lb = t;
-                }
-                int32_t* hdr = send.data() + n_max;
-                hdr[0] = lb >= 0 ? 1 : 0;
-                if (lb >= 0) {
-                    int32_t len = 0, st = 0;
-                    u64 sd64 = 0;
-                    CU(cudaMemcpyAsync(&len, P.len.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
-                    CU(cudaMemcpyAsync(&st, P.strat.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
-                    CU(cudaMemcpyAsync(&sd64, P.seed.as<u64>() + lb, 8, cudaMemcpyDeviceToHost, ctx->stream));
-                    CU(cudaStreamSynchronize(ctx->stream));
-                    hdr[1] = p0 + lb;
-                    hdr[2] = len;
-                    hdr[3] = st;
-                    std::memcpy(&hdr[4], &sd64, 8);
-                    CU(cudaMemcpyAsync(hdr + 6, P.subs.as<u32>() + size_t(lb) * size_t(P.sub_cap), 4 * size_t(len),
-                                       cudaMemcpyDeviceToHost, ctx->stream));
-                    CU(cudaStreamSynchronize(ctx->stream));
-                }
-                if (ctx->allgather(send.data(), recv.data(), send.size() * 4, ctx->ag_user) != 0)
-                    return fail(TCSE_ENCCL, "exchange: allgather failed");
-                std::vector<int32_t> gcost((size_t)n);
-                int best_r = -1, best_p = -1, best_c = 0;
-                for (int r = 0; r < world; ++r) {
-                    const int32_t* rr = recv.data() + size_t(r) * size_t(words);
-                    for (int t = 0; t < part(r + 1) - part(r); ++t)
-                        gcost[size_t(part(r) + t)] = rr[t];
-                    const int32_t* h = rr + n_max;
-                    if (h[0] && (best_r < 0 || h[1 + 0] >= 0)) {
-                        const int bp = h[1], bc = rr[bp - part(r)];
-                        if (best_r < 0 || bc < best_c || (bc == best_c && bp < best_p)) {
-                            best_r = r;
-                            best_p = bp;
-                            best_c = bc;
-                        }
-                    }
-                }
-                const int32_t* h = recv.data() + size_t(best_r) * size_t(words) + n_max;
-                // stage: [len, strategy, seed(2 words)] + keys
-                std::vector<int32_t> stage(size_t(4 + P.sub_cap), 0);
-                stage[0] = h[2];
-                stage[1] = h[3];
-                stage[2] = h[4];
-                stage[3] = h[5];
-                std::memcpy(stage.data() + 4, h + 6, 4 * size_t(h[2]));
-                CU(cudaMemcpyAsync(P.gcost.p, gcost.data(), 4 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
-                CU(cudaMemcpyAsync(P.stage.p, stage.data(), 4 * stage.size(), cudaMemcpyHostToDevice, ctx->stream));
-                R.costs = P.gcost.as<int32_t>();
-                R.rec_base = best_p;
-                R.rec_n = 1;
-                R.lens = P.stage.as<int32_t>();
-                R.strategies = P.stage.as<int32_t>() + 1;
-                R.seeds = reinterpret_cast<const u64*>(P.stage.as<int32_t>() + 2);
-                R.subs = P.stage.as<u32>() + 4;
-            }
-            RL.r[RL.nsys++] = R;
-        }
-        CU(launch_reduce(RL, hist_n, ctx->stream));
-        // ---- host: incumbent bookkeeping (patience, callback)
-        std::vector<IncState> st(act.size());
-        for (size_t a = 0; a < act.size(); ++a)
-            CU(cudaMemcpyAsync(&st[a], pool[size_t(act[a])].inc.p, sizeof(IncState), cudaMemcpyDeviceToHost,
-                               ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        exchange_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx).count();
-        rc = check_err(ctx);
-        if (rc)
-            return rc;
-        if (blocks > 0) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
-            kernel_ms += ms;
-        }
-        bool stop_all = false;
-        for (size_t a = 0; a < act.size(); ++a) {
-            const int s = act[a];
-            hinc[size_t(s)] = st[a];
-            iters[size_t(s)] = iteration;
-            if (st[a].improved) {
-                unchanged[size_t(s)] = 0;
-                hinc_keys[size_t(s)].resize(size_t(std::max(st[a].len, 1)));
-                if (cb) {
-                    CU(cudaMemcpyAsync(hinc_keys[size_t(s)].data(), pool[size_t(s)].inc_keys.p, 4 * size_t(st[a].len),
-                                       cudaMemcpyDeviceToHost, ctx->stream));
-                    CU(cudaStreamSynchronize(ctx->stream));
-                }
-            } else {
-                ++unchanged[size_t(s)];
-            }
-            if (cb) {
-                auto& pairs = hinc_pairs[size_t(s)];
-                if (st[a].improved || pairs.empty()) {
-                    pairs.resize(size_t(std::max(st[a].len, 1)));
-                    for (int t = 0; t < st[a].len; ++t)
-                        pairs[size_t(t)] = key_pair(hinc_keys[size_t(s)][size_t(t)]);
-                }
-                tcse_record r;
-                r.subs = pairs.data();
-                r.cap = st[a].len;
-                r.n_subs = st[a].len;
-                r.cost = st[a].cost;
-                r.strategy = st[a].strategy;
-                r.seed = st[a].seed;
-                if (cb(s, iteration, &r, user) != 0)
-                    stop_all = true;
-            }
-            if (unchanged[size_t(s)] >= cfg->patience ||
-                (cfg->max_iterations > 0 && iteration >= cfg->max_iterations))
-                active[size_t(s)] = 0;
-        }
-        if (stop_all)
-            break;
+// all-gather this rank's costs and best record; stage the global view
+int exchange(tcse_search* S, int s, ReduceDesc* R) {
+    tcse_ctx* ctx = S->ctx;
+    Pool& P = S->pool[size_t(s)];
+    const int n = S->n, world = ctx->world, n_local = S->n_local, p0 = S->p0;
+    auto part = [&](int r) { return int((long long)n * r / world); };
+    const int n_max = (n + world - 1) / world + 1;
+    const int words = n_max + 6 + P.sub_cap;
+    std::vector<int32_t> send(size_t(words), 0), recv(size_t(words) * size_t(world), 0);
+    std::vector<int32_t> c(size_t(std::max(n_local, 1)));
+    CU(cudaMemcpyAsync(c.data(), P.cost.p, 4 * size_t(n_local), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    int rc = check_err(ctx);
+    if (rc)
+        return rc;
+    int lb = -1;
+    for (int t = 0; t < n_local; ++t) {
+        send[size_t(t)] = c[size_t(t)];
+        if (lb < 0 || c[size_t(t)] < c[size_t(lb)])
+            lb = t;
     }
-    // ---- results
-    uint64_t steps = 0;
-    for (int s = 0; s < n_systems; ++s) {
-        const IncState& I = hinc[size_t(s)];
-        if (I.len > best[s].cap)
-            return fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < %d", best[s].cap, I.len);
-        std::vector<u32> k(size_t(std::max(I.len, 1)));
-        CU(cudaMemcpyAsync(k.data(), pool[size_t(s)].inc_keys.p, 4 * size_t(I.len), cudaMemcpyDeviceToHost, ctx->stream));
-        IncState fin;
-        CU(cudaMemcpyAsync(&fin, pool[size_t(s)].inc.p, sizeof fin, cudaMemcpyDeviceToHost, ctx->stream));
+    int32_t* hdr = send.data() + n_max;
+    hdr[0] = lb >= 0 ? 1 : 0;
+    if (lb >= 0) {
+        int32_t len = 0, st = 0;
+        u64 sd64 = 0;
+        CU(cudaMemcpyAsync(&len, P.len.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(&st, P.strat.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaMemcpyAsync(&sd64, P.seed.as<u64>() + lb, 8, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
-        for (int t = 0; t < I.len; ++t)
-            best[s].subs[t] = key_pair(k[size_t(t)]);
-        best[s].n_subs = I.len;
-        best[s].cost = I.cost;
-        best[s].strategy = I.strategy;
-        best[s].seed = I.seed;
+        hdr[1] = p0 + lb;
+        hdr[2] = len;
+        hdr[3] = st;
+        std::memcpy(&hdr[4], &sd64, 8);
+        CU(cudaMemcpyAsync(hdr + 6, P.subs.as<u32>() + size_t(lb) * size_t(P.sub_cap), 4 * size_t(len),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    if (ctx->allgather(send.data(), recv.data(), send.size() * 4, ctx->ag_user) != 0)
+        return fail(TCSE_ENCCL, "exchange: allgather failed");
+    std::vector<int32_t> gcost((size_t)n);
+    int best_r = -1, best_p = -1, best_c = 0;
+    for (int r = 0; r < world; ++r) {
+        const int32_t* rr = recv.data() + size_t(r) * size_t(words);
+        for (int t = 0; t < part(r + 1) - part(r); ++t)
+            gcost[size_t(part(r) + t)] = rr[t];
+        const int32_t* h = rr + n_max;
+        if (h[0]) {
+            const int bp = h[1], bc = rr[bp - part(r)];
+            if (best_r < 0 || bc < best_c || (bc == best_c && bp < best_p)) {
+                best_r = r;
+                best_p = bp;
+                best_c = bc;
+            }
+        }
+    }
+    if (best_r < 0)
+        return fail(TCSE_ENCCL, "exchange: no rank reported a record");
+    const int32_t* h = recv.data() + size_t(best_r) * size_t(words) + n_max;
+    std::vector<int32_t> stage(size_t(4 + P.sub_cap), 0);
+    stage[0] = h[2];
+    stage[1] = h[3];
+    stage[2] = h[4];
+    stage[3] = h[5];
+    std::memcpy(stage.data() + 4, h + 6, 4 * size_t(h[2]));
+    CU(cudaMemcpyAsync(P.gcost.p, gcost.data(), 4 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(P.stage.p, stage.data(), 4 * stage.size(), cudaMemcpyHostToDevice, ctx->stream));
+    S->h2d += 4 * uint64_t(n) + 4 * stage.size();
+    S->d2h += 4 * uint64_t(n_local) + 16 + 4 * uint64_t(h[2]);
+    R->costs = P.gcost.as<int32_t>();
+    R->rec_base = best_p;
+    R->rec_n = 1;
+    R->lens = P.stage.as<int32_t>();
+    R->strategies = P.stage.as<int32_t>() + 1;
+    R->seeds = reinterpret_cast<const u64*>(P.stage.as<int32_t>() + 2);
+    R->subs = P.stage.as<u32>() + 4;
+    return TCSE_OK;
+}
+
+int search_step(tcse_search* S, int32_t* n_active) {
+    tcse_ctx* ctx = S->ctx;
+    int rc = TCSE_OK;
+    std::vector<int> act;
+    for (int s = 0; s < S->n_systems; ++s)
+        if (S->active[size_t(s)])
+            act.push_back(s);
+    if (act.empty() || S->stopped) {
+        *n_active = 0;
+        return TCSE_OK;
+    }
+    CU(cudaSetDevice(ctx->device));
+    const int iteration = ++S->iteration;
+    // ---- K1: every local process of every active system, one launch
+    LaunchDesc L;
+    std::memset(&L, 0, sizeof L);
+    int blocks = 0;
+    for (int s : act) {
+        const DevSys& d = S->dev[size_t(s)];
+        Pool& P = S->pool[size_t(s)];
+        SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
+        sd.mode = kModeSearch;
+        sd.base_keys = d.keys.as<u32>();
+        sd.base_cnts = d.cnts.as<u16>();
+        sd.base_m = d.base_m;
+        sd.n_local = S->n_local;
+        sd.p0 = S->p0;
+        sd.block_begin = blocks;
+        sd.master_seed = S->cfg.master_seed;
+        sd.salt = S->salts[size_t(s)];
+        sd.iteration = iteration;
+        sd.forced = S->cfg.forced_strategy;
+        for (int k = 0; k < 7; ++k)
+            sd.weights[k] = S->cfg.strategy_weights[k];
+        sd.weight_total = S->weight_total;
+        for (int k = 0; k < 4; ++k)
+            sd.mix[k] = S->cfg.mix_weights[k];
+        sd.reinit = iteration >= 2 ? P.reinit.as<u8>() + S->p0 : nullptr;
+        sd.inc_keys = P.inc_keys.as<u32>();
+        sd.inc_len = S->hinc[size_t(s)].len;
+        sd.out_cost = P.cost.as<int32_t>();
+        sd.out_len = P.len.as<int32_t>();
+        sd.out_own = P.own.as<int32_t>();
+        sd.out_strategy = P.strat.as<int32_t>();
+        sd.out_seed = P.seed.as<u64>();
+        sd.out_wops = P.wops.as<u64>();
+        sd.out_subs = P.subs.as<u32>();
+        L.sys[L.nsys++] = sd;
+        blocks += S->n_local;
+    }
+    L.total_blocks = blocks;
+    CU(cudaEventRecord(S->es0, ctx->stream));
+    if (blocks > 0) {
+        CU(cudaEventRecord(ctx->ev0, ctx->stream));
+        CU(launch_search(L, S->Wmax, S->nt, S->smem, ctx->stream));
+        CU(cudaEventRecord(ctx->ev1, ctx->stream));
+        ++S->launches;
+        S->processes += uint64_t(blocks);
+    }
+    const auto tx = std::chrono::steady_clock::now();
+    // ---- K2 (+ cross-rank exchange): incumbent pool update, next reinit set
+    ReduceLaunch RL;
+    std::memset(&RL, 0, sizeof RL);
+    for (int s : act) {
+        Pool& P = S->pool[size_t(s)];
+        ReduceDesc R;
+        std::memset(&R, 0, sizeof R);
+        R.n = S->n;
+        R.costs = P.cost.as<int32_t>();
+        R.rec_base = 0;
+        R.rec_n = S->n;
+        R.lens = P.len.as<int32_t>();
+        R.strategies = P.strat.as<int32_t>();
+        R.seeds = P.seed.as<u64>();
+        R.subs = P.subs.as<u32>();
+        R.stride = P.sub_cap;
+        R.own = P.own.as<int32_t>();
+        R.own_len = P.len.as<int32_t>();
+        R.own_wops = P.wops.as<u64>();
+        R.own_n = S->n_local;
+        R.inc = P.inc.as<IncState>();
+        R.inc_keys = P.inc_keys.as<u32>();
+        R.reinit_next = P.reinit.as<u8>();
+        R.fraction = S->cfg.reinit_fraction;
+        R.hist_n = S->hist_n;
+        if (ctx->world > 1 && (rc = exchange(S, s, &R)))
+            return rc;
+        RL.r[RL.nsys++] = R;
+    }
+    CU(launch_reduce(RL, S->hist_n, ctx->stream));
+    CU(cudaEventRecord(S->es1, ctx->stream));
+    std::vector<IncState> st(act.size());
+    for (size_t a = 0; a < act.size(); ++a)
+        CU(cudaMemcpyAsync(&st[a], S->pool[size_t(act[a])].inc.p, sizeof(IncState), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    S->d2h += sizeof(IncState) * act.size();
+    CU(cudaStreamSynchronize(ctx->stream));
+    S->exchange_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx).count();
+    rc = check_err(ctx);
+    if (rc)
+        return rc;
+    float ms = 0.f;
+    if (blocks > 0 && cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess)
+        S->kernel_ms += ms;
+    if (cudaEventElapsedTime(&ms, S->es0, S->es1) == cudaSuccess)
+        S->step_ms += ms;
+    // ---- host: patience (parallel_search.hpp:261-270) and on_iteration
+    for (size_t a = 0; a < act.size(); ++a) {
+        const int s = act[a];
+        S->hinc[size_t(s)] = st[a];
+        S->iters[size_t(s)] = iteration;
+        if (st[a].improved) {
+            S->unchanged[size_t(s)] = 0;
+            S->hinc_keys[size_t(s)].resize(size_t(std::max(st[a].len, 1)));
+            if (S->cb) {
+                CU(cudaMemcpyAsync(S->hinc_keys[size_t(s)].data(), S->pool[size_t(s)].inc_keys.p,
+                                   4 * size_t(st[a].len), cudaMemcpyDeviceToHost, ctx->stream));
+                CU(cudaStreamSynchronize(ctx->stream));
+                S->d2h += 4 * uint64_t(st[a].len);
+            }
+        } else {
+            ++S->unchanged[size_t(s)];
+        }
+        if (S->cb) {
+            auto& pairs = S->hinc_pairs[size_t(s)];
+            if (st[a].improved || pairs.empty()) {
+                pairs.resize(size_t(std::max(st[a].len, 1)));
+                for (int t = 0; t < st[a].len; ++t)
+                    pairs[size_t(t)] = key_pair(S->hinc_keys[size_t(s)][size_t(t)]);
+            }
+            tcse_record r;
+            r.subs = pairs.data();
+            r.cap = st[a].len;
+            r.n_subs = st[a].len;
+            r.cost = st[a].cost;
+            r.strategy = st[a].strategy;
+            r.seed = st[a].seed;
+            if (S->cb(s, iteration, &r, S->user) != 0)
+                S->stopped = true;
+        }
+        if (S->unchanged[size_t(s)] >= S->cfg.patience ||
+            (S->cfg.max_iterations > 0 && iteration >= S->cfg.max_iterations))
+            S->active[size_t(s)] = 0;
+    }
+    int left = 0;
+    for (int s = 0; s < S->n_systems; ++s)
+        left += S->active[size_t(s)];
+    *n_active = S->stopped ? 0 : left;
+    return TCSE_OK;
+}
+
+int search_result(tcse_search* S, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
+    tcse_ctx* ctx = S->ctx;
+    CU(cudaSetDevice(ctx->device));
+    uint64_t steps = 0, replayed = 0, wops = 0;
+    for (int s = 0; s < S->n_systems; ++s) {
+        const IncState& I = S->hinc[size_t(s)];
+        IncState fin;
+        CU(cudaMemcpyAsync(&fin, S->pool[size_t(s)].inc.p, sizeof fin, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<u32> k(size_t(std::max(I.len, 1)));
+        if (best) {
+            if (I.len > best[s].cap)
+                return fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < %d", best[s].cap, I.len);
+            CU(cudaMemcpyAsync(k.data(), S->pool[size_t(s)].inc_keys.p, 4 * size_t(I.len), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+        }
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (best) {
+            for (int t = 0; t < I.len; ++t)
+                best[s].subs[t] = key_pair(k[size_t(t)]);
+            best[s].n_subs = I.len;
+            best[s].cost = I.cost;
+            best[s].strategy = I.strategy;
+            best[s].seed = I.seed;
+            S->d2h += 4 * uint64_t(I.len);
+        }
         if (iterations)
-            iterations[s] = iters[size_t(s)];
+            iterations[s] = S->iters[size_t(s)];
         steps += fin.steps;
+        replayed += fin.replayed;
+        wops += fin.wops;
     }
     if (stats) {
         std::memset(stats, 0, sizeof *stats);
         stats->steps = steps;
-        stats->processes = processes;
-        stats->launches = launches;
-        stats->iterations = iteration;
-        stats->kernel_ms = kernel_ms;
-        stats->exchange_ms = exchange_ms;
-        stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        stats->replayed = replayed;
+        stats->wops = wops;
+        stats->processes = S->processes;
+        stats->launches = S->launches;
+        stats->iterations = S->iteration;
+        stats->kernel_ms = S->kernel_ms;
+        stats->step_ms = S->step_ms;
+        stats->exchange_ms = S->exchange_ms;
+        stats->h2d_bytes = S->h2d;
+        stats->d2h_bytes = S->d2h;
+        stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - S->t0).count();
     }
     return TCSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tcse_microbench_wordops_impl(int device, double* gops);
+
+int tcse_microbench_wordops(tcse_ctx* ctx, double* gops) {
+    if (!ctx || !gops)
+        return fail(TCSE_EINVAL, "tcse_microbench_wordops: bad argument");
+    const int rc = tcse_microbench_wordops_impl(ctx->device, gops);
+    return rc ? fail(rc, "microbenchmark failed") : TCSE_OK;
+}
+
+int tcse_search_create(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems, const tcse_search_config* cfg,
+                       const uint64_t* salts, tcse_iter_cb cb, void* user, tcse_search** out) {
+    if (!out)
+        return fail(TCSE_EINVAL, "tcse_search_create: null output");
+    *out = nullptr;
+    auto* S = new tcse_search;
+    const int rc = search_init(S, ctx, n_systems, systems, cfg, salts, cb, user);
+    if (rc) {
+        delete S;
+        return rc;
+    }
+    *out = S;
+    return TCSE_OK;
+}
+
+int tcse_search_step(tcse_search* S, int32_t* n_active) {
+    if (!S || !n_active)
+        return fail(TCSE_EINVAL, "tcse_search_step: bad argument");
+    return search_step(S, n_active);
+}
+
+int tcse_search_result(tcse_search* S, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
+    if (!S)
+        return fail(TCSE_EINVAL, "tcse_search_result: bad argument");
+    return search_result(S, best, iterations, stats);
+}
+
+void tcse_search_destroy(tcse_search* S) {
+    if (S) {
+        cudaSetDevice(S->ctx->device);
+        delete S;
+    }
+}
+
+int tcse_optimize_systems(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
+                          const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb,
+                          void* user, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
+    if (!best)
+        return fail(TCSE_EINVAL, "optimize_systems: null result");
+    tcse_search* S = nullptr;
+    int rc = tcse_search_create(ctx, n_systems, systems, cfg, salts, cb, user, &S);
+    if (rc)
+        return rc;
+    for (int s = 0; s < n_systems; ++s)
+        if (best[s].cap < S->dev[size_t(s)].h.naive) {
+            rc = fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < naive cost %d", best[s].cap,
+                      S->dev[size_t(s)].h.naive);
+            tcse_search_destroy(S);
+            return rc;
+        }
+    int32_t left = 1;
+    while (left > 0 && rc == TCSE_OK)
+        rc = search_step(S, &left);
+    if (rc == TCSE_OK)
+        rc = search_result(S, best, iterations, stats);
+    tcse_search_destroy(S);
+    return rc;
 }
 
 int tcse_optimize_system(tcse_ctx* ctx, const tcse_system* sys, const tcse_search_config* cfg, uint64_t stream_salt,

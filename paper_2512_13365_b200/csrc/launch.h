@@ -33,6 +33,7 @@ enum Mode : int32_t {
 struct SysDesc {
     // problem (base state, shared read-only by every block of the system)
     int32_t n_x, n_e, naive;
+    int32_t words;    // ceil(n_e / 64): words a mask needs (the launch may use more)
     int32_t vcap;     // variable capacity = n_x + naive
     int32_t mcap;     // candidate capacity (<= pair occurrences / 2)
     int32_t sub_cap;  // record stride (u32 keys) = naive + 1
@@ -77,6 +78,7 @@ struct SysDesc {
     int32_t* out_own;  // substitutions selected by this process (steps)
     int32_t* out_strategy;
     u64* out_seed;
+    u64* out_wops;  // algorithmic word-ops per process (roofline), may be null
     u32* out_subs;  // [n_local][sub_cap]
     u64* trace;     // [n_local][trace_stride] or null
     int32_t trace_stride;
@@ -103,6 +105,7 @@ struct IncState {
     int32_t reserved;
     u64 steps;         // accumulated selected substitutions
     u64 replayed;
+    u64 wops;          // accumulated algorithmic word-ops
 };
 
 // smem bytes one block of this system needs at launch word count W

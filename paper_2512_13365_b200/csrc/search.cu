@@ -227,6 +227,8 @@ struct Proc {
     int n_rec;  // record entries written (prefix included in search mode)
     int n_own;  // substitutions selected by this process
     int mti;    // mt19937_64 position (312 = twist pending)
+    u64 wops;   // algorithmic word-intersections (SURVEY.md 8(d) model), thread 0
+    u32 last_coins;  // coins drawn by the last gi selection (sum of deg)
 
     __device__ Proc(const SysDesc& s, int lp_, unsigned char* smem) : sd(s), lp(lp_) {
         tid = threadIdx.x;
@@ -664,6 +666,7 @@ struct Proc {
         }
         if (tid == 0)
             qbase[m] = D;
+        last_coins = D;
         __syncthreads();
         double best_s = -1.0;
         int best_q = 0x7fffffff;
@@ -966,6 +969,8 @@ __global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ Laun
     pr.n_rec = 0;
     pr.n_own = 0;
     pr.mti = 312;
+    pr.wops = 0;
+    pr.last_coins = 0;
     if (sd.base_keys) {
         pr.m = sd.base_m;
     } else {
@@ -1042,6 +1047,17 @@ __global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ Laun
             default: pick = pr.sel_gp(alpha); break;
         }
         const u32 q = pr.keys[pr.cur][pick];
+        {
+            // recount 12(V-1)W_E + substitution 8 W_E + selection
+            // (m for g/ga/wr/gr; m + sum deg for gi; m (V-2) 4 W_E for gp)
+            const u64 Vt = u64(pr.V), mt_ = u64(pr.m), we = u64(sd.words);
+            u64 sel = mt_;
+            if (strat == TCSE_GREEDY_INTERSECTIONS && alpha != 0.0)
+                sel += pr.last_coins;
+            if (strat == TCSE_GREEDY_POTENTIAL && alpha != 0.0)
+                sel += mt_ * (Vt - 2) * 4 * we;
+            pr.wops += 12 * (Vt - 1) * we + 8 * we + sel;
+        }
         pr.apply(q);
         pr.update(q);
         if (tid == 0) {
@@ -1061,6 +1077,8 @@ __global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ Laun
         sd.out_own[lp] = pr.n_own;
         sd.out_strategy[lp] = strategy;
         sd.out_seed[lp] = seed;
+        if (sd.out_wops)
+            sd.out_wops[lp] = pr.wops;
     }
     (void)NW;
 }
@@ -1077,7 +1095,9 @@ struct ReduceDesc {
     const u64* seeds;
     const u32* subs;
     int32_t stride;
-    const int32_t* own;  // [own_n] selected-substitution counts of this rank's processes
+    const int32_t* own;      // [own_n] selected-substitution counts of this rank's processes
+    const int32_t* own_len;  // [own_n] their record lengths (prefix included)
+    const u64* own_wops;     // [own_n] algorithmic word-ops
     int32_t own_n;
     IncState* inc;
     u32* inc_keys;
@@ -1099,6 +1119,8 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ u64 s_min[32];
     __shared__ u64 s_sum[32];
+    __shared__ u64 s_rep[32];
+    __shared__ u64 s_wop[32];
     __shared__ u32 s_red[34];
     __shared__ int s_thr[2];
     // argmin over (cost, process id) — lowest index wins ties (255-260)
@@ -1106,25 +1128,35 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
     u64 steps = 0;
     for (int p = tid; p < R.n; p += kRedNT)
         best = min(best, (u64(u32(R.costs[p])) << 32) | u64(u32(p)));
-    for (int p = tid; p < R.own_n; p += kRedNT)
+    u64 replayed = 0, wops = 0;
+    for (int p = tid; p < R.own_n; p += kRedNT) {
         steps += u64(R.own[p]);
+        replayed += u64(R.own_len[p] - R.own[p]);
+        wops += R.own_wops[p];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         best = min(best, __shfl_down_sync(FULLMASK, best, o));
         steps += __shfl_down_sync(FULLMASK, steps, o);
+        replayed += __shfl_down_sync(FULLMASK, replayed, o);
+        wops += __shfl_down_sync(FULLMASK, wops, o);
     }
     if (lane == 0) {
         s_min[warp] = best;
         s_sum[warp] = steps;
+        s_rep[warp] = replayed;
+        s_wop[warp] = wops;
     }
     for (int v = tid; v < R.hist_n; v += kRedNT)
         hist[v] = 0;
     __syncthreads();
     if (tid == 0) {
-        u64 b = s_min[0], st = 0;
+        u64 b = s_min[0], st = 0, rp = 0, wo = 0;
         for (int w = 0; w < kRedNT / 32; ++w) {
             b = min(b, s_min[w]);
             st += s_sum[w];
+            rp += s_rep[w];
+            wo += s_wop[w];
         }
         const int bp = int(b & 0xffffffffu);
         const int bc = int(b >> 32);
@@ -1132,6 +1164,8 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
         inc->best_p = bp;
         inc->best_cost = bc;
         inc->steps += st;
+        inc->replayed += rp;
+        inc->wops += wo;
         if (!inc->have || bc < inc->cost) {  // strictly better (261-266)
             inc->have = 1;
             inc->cost = bc;
