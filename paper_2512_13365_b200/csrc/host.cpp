@@ -207,11 +207,12 @@ struct tcse_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t owned_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    int nt = 128;
+    int nt = 64;
     int rank = 0, world = 1;
     tcse_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
     DBuf err;  // int32 err + err_pos
+    DBuf slots, rng;  // prep_kernel -> search_kernel hand-off
 };
 
 // one system prepared on the device
@@ -224,10 +225,16 @@ struct DevSys {
 
 namespace {
 
-int prepare(tcse_ctx* ctx, const tcse_system* s, int W, DevSys* d) {
+// extra_vars: fresh variables a caller-supplied prefix may add beyond the
+// search bound.  Every search substitution replaces c >= 2 occurrences and
+// the total term count can drop by at most naive (rows never empty), so a
+// search creates at most naive/2 fresh variables; an arbitrary replayed
+// prefix may use c = 1 pairs, hence the extra allowance.
+int prepare(tcse_ctx* ctx, const tcse_system* s, int W, DevSys* d, int extra_vars = 0) {
     int rc = validate_system(s, &d->h);
     if (rc)
         return rc;
+    d->h.vcap = d->h.n_x + d->h.naive / 2 + extra_vars + 1;
     d->W = W;
     const auto masks = pack_masks(d->h, W);
     CU(d->masks.reserve(std::max<size_t>(8, masks.size() * 8)));
@@ -238,11 +245,50 @@ int prepare(tcse_ctx* ctx, const tcse_system* s, int W, DevSys* d) {
     return TCSE_OK;
 }
 
-int smem_for(const tcse_ctx* ctx, int W, const std::vector<DevSys*>& sys) {
-    int64_t mx = 0;
-    for (auto* d : sys)
-        mx = std::max(mx, smem_bytes(W, d->h.vcap, d->h.mcap, ctx->nt));
+// block size the kernel is instantiated for at this word count
+int pick_nt(tcse_ctx* ctx, int W) {
+    int nt = ctx->nt;
+    if (nt == 32 && W != 1)
+        nt = 64;
+    if (nt == 64 && W > 2)
+        nt = 128;
+    if (nt == 256 && W != 1 && W != 3)
+        nt = 128;
+    return nt;
+}
+
+int coin_words_for(const HostSys& h) {
+    // gi coin bits: all coins of a step fit for typical states (sum of
+    // degrees), else the kernel evaluates gi densely in chunks
+    const long long want = (long long)h.mcap * 24 / 32 + 64;
+    return int(std::min<long long>(std::max<long long>(want, 256), 2048));
+}
+
+// gi evaluation form: the O(deg) walk pays off once candidate lists are long
+int gi_dense_for(const HostSys& h) {
+    const int forced = env_int("TCSE_GI_DENSE", -1);
+    if (forced >= 0)
+        return forced ? 1 : 0;
+    return h.mcap <= 640 ? 1 : 0;
+}
+
+int smem_for(int nt, int W, const std::vector<DevSys*>& sys) {
+    u32 mx = 0;
+    for (auto* d : sys) {
+        Lay L;
+        mx = std::max(mx, carve(&L, W, nt, d->h.vcap, d->h.mcap, d->h.n_e, coin_words_for(d->h), gi_dense_for(d->h)));
+    }
     return int(mx);
+}
+
+// slot records + seeded mt19937_64 states for `blocks` processes
+int attach_prep(tcse_ctx* ctx, LaunchDesc* L) {
+    const size_t b = size_t(std::max(L->total_blocks, 1));
+    CU(ctx->slots.reserve(b * sizeof(SlotRec)));
+    CU(ctx->rng.reserve(b * 312 * 8));
+    L->slots = ctx->slots.as<SlotRec>();
+    L->rng = ctx->rng.as<u64>();
+    return TCSE_OK;
 }
 
 int check_err(tcse_ctx* ctx) {
@@ -265,9 +311,11 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.n_e = d.h.n_e;
     sd.naive = d.h.naive;
     sd.words = d.h.w_need;
+    sd.coin_words = coin_words_for(d.h);
+    sd.gi_dense = gi_dense_for(d.h);
     sd.vcap = d.h.vcap;
     sd.mcap = d.h.mcap;
-    sd.sub_cap = d.h.naive + 1;
+    sd.sub_cap = d.h.naive / 2 + 1;
     sd.base_masks = d.masks.as<u64>();
     sd.forced = -1;
     sd.err = err;
@@ -300,7 +348,10 @@ int run_dump(tcse_ctx* ctx, DevSys& d, const u32* d_prefix, int n_prefix, int mi
     sd.dump_n = dn.as<int32_t>();
     L.sys[0] = sd;
     std::vector<DevSys*> v{&d};
-    CU(launch_search(L, d.W, ctx->nt, smem_for(ctx, d.W, v), ctx->stream));
+    int prc = attach_prep(ctx, &L);
+    if (prc)
+        return prc;
+    CU(launch_search(L, d.W, pick_nt(ctx, d.W), smem_for(pick_nt(ctx, d.W), d.W, v), ctx->stream));
     int rc = check_err(ctx);
     if (rc)
         return rc;
@@ -374,14 +425,7 @@ int validate_mix(const double* mix) {
     return TCSE_OK;
 }
 
-int pick_nt(tcse_ctx* ctx, int W) {
-    int nt = ctx->nt;
-    if (W > 2 && nt == 64)
-        nt = 128;
-    if (nt == 256 && W != 1 && W != 3)
-        nt = 128;
-    return nt;
-}
+
 
 }  // namespace
 
@@ -441,9 +485,9 @@ tcse_ctx* tcse_create(int32_t device) {
     }
     auto* ctx = new tcse_ctx;
     ctx->device = device;
-    ctx->nt = env_int("TCSE_NT", 128);
-    if (ctx->nt != 64 && ctx->nt != 128 && ctx->nt != 256)
-        ctx->nt = 128;
+    ctx->nt = env_int("TCSE_NT", 64);
+    if (ctx->nt != 32 && ctx->nt != 64 && ctx->nt != 128 && ctx->nt != 256)
+        ctx->nt = 64;
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
         ctx->err.reserve(8) != cudaSuccess) {
@@ -498,7 +542,7 @@ int tcse_count_pairs(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* pre
     int rc = validate_system(sys, &probe);
     if (rc)
         return rc;
-    rc = prepare(ctx, sys, launch_words(probe.w_need), &d);
+    rc = prepare(ctx, sys, launch_words(probe.w_need), &d, n_prefix);
     if (rc)
         return rc;
     rc = base_candidates(ctx, d);
@@ -560,7 +604,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     if (rc)
         return rc;
     const int W = launch_words(probe.w_need);
-    rc = prepare(ctx, sys, W, &d);
+    rc = prepare(ctx, sys, W, &d, n_prefix);
     if (rc)
         return rc;
     rc = base_candidates(ctx, d);
@@ -570,7 +614,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     rc = upload_pairs(ctx, prefix, n_prefix, &dpre);
     if (rc)
         return rc;
-    const int sub_cap = d.h.naive + 1;
+    const int sub_cap = d.h.naive / 2 + 1;
     CU(dcfg.reserve(sizeof(tcse_process_config) * size_t(n)));
     CU(cudaMemcpyAsync(dcfg.p, cfgs, sizeof(tcse_process_config) * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
     CU(dcost.reserve(4 * size_t(n)));
@@ -606,8 +650,11 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     sd.trace_stride = trace_stride;
     L.sys[0] = sd;
     std::vector<DevSys*> v{&d};
+    rc = attach_prep(ctx, &L);
+    if (rc)
+        return rc;
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
-    CU(launch_search(L, W, pick_nt(ctx, W), smem_for(ctx, W, v), ctx->stream));
+    CU(launch_search(L, W, pick_nt(ctx, W), smem_for(pick_nt(ctx, W), W, v), ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
     rc = check_err(ctx);
     if (rc)
@@ -741,13 +788,13 @@ int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_sys
             return rc;
         dptr.push_back(&d);
     }
-    S->smem = smem_for(ctx, S->Wmax, dptr);
+    S->smem = smem_for(S->nt, S->Wmax, dptr);
     if (S->smem > 227 * 1024 - 1024)
         return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", S->smem);
     for (int s = 0; s < n_systems; ++s) {
         Pool& P = S->pool[size_t(s)];
         const DevSys& d = S->dev[size_t(s)];
-        P.sub_cap = d.h.naive + 1;
+        P.sub_cap = d.h.naive / 2 + 1;
         const size_t nl = size_t(std::max(S->n_local, 1));
         CU(P.cost.reserve(4 * nl));
         CU(P.len.reserve(4 * nl));
@@ -913,6 +960,8 @@ int search_step(tcse_search* S, int32_t* n_active) {
         blocks += S->n_local;
     }
     L.total_blocks = blocks;
+    if ((rc = attach_prep(ctx, &L)))
+        return rc;
     CU(cudaEventRecord(S->es0, ctx->stream));
     if (blocks > 0) {
         CU(cudaEventRecord(ctx->ev0, ctx->stream));

@@ -34,6 +34,8 @@ struct SysDesc {
     // problem (base state, shared read-only by every block of the system)
     int32_t n_x, n_e, naive;
     int32_t words;    // ceil(n_e / 64): words a mask needs (the launch may use more)
+    int32_t coin_words;  // gi coin buffer (u32 words) per block
+    int32_t gi_dense;    // 1: gi by the reference's O(m) loop per candidate; 0: O(deg) walk
     int32_t vcap;     // variable capacity = n_x + naive
     int32_t mcap;     // candidate capacity (<= pair occurrences / 2)
     int32_t sub_cap;  // record stride (u32 keys) = naive + 1
@@ -86,9 +88,22 @@ struct SysDesc {
     int32_t* err_pos;
 };
 
+// per-process configuration handed from the prep kernel to the search kernel
+struct SlotRec {
+    int32_t strategy;
+    int32_t reinit;  // restart from an incumbent prefix
+    int32_t rng;     // the process draws from its mt19937_64 stream
+    int32_t pad;
+    double alpha, beta, p_greedy;
+    u64 seed;
+    double mix[4];
+};
+
 struct LaunchDesc {
     int32_t nsys;
     int32_t total_blocks;
+    SlotRec* slots;  // [total_blocks]
+    u64* rng;        // [total_blocks][312] seeded mt19937_64 states
     SysDesc sys[kMaxSys];
 };
 
@@ -108,25 +123,86 @@ struct IncState {
     u64 wops;          // accumulated algorithmic word-ops
 };
 
-// smem bytes one block of this system needs at launch word count W
-inline int64_t smem_bytes(int W, int vcap, int mcap, int nt) {
-    auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
-    int64_t b = 0;
-    b += al(int64_t(vcap) * 2 * W * 8);           // masks
-    b += al(int64_t(mcap) * 4) * 2;               // keys x2
-    b += al(int64_t(mcap) * 2) * 2;               // cnts x2
-    int64_t upd = al(int64_t(mcap) * 2)           // tcnt
-                + al(int64_t(vcap + 1) * 2) * 2   // ncp, ncn
-                + al(int64_t(mcap) * 4)           // aux
-                + al(int64_t(vcap + 2) * 4);      // newexcl
-    int64_t gi = al(int64_t(kCoinWords) * 4)      // coin bits
-               + al(int64_t(mcap + 1) * 4)        // qbase
-               + al(int64_t(vcap + 1) * 4)        // nvar
-               + al(int64_t(mcap) * 8) * 2;       // wd, wb
-    b += upd > gi ? upd : gi;
-    b += 312 * 8;                                 // mt19937_64 state
-    b += al(int64_t(nt / 32 + 2) * 8) * 3;        // reduction scratch
-    return b;
+// Shared-memory carve of one process (block).  Byte offsets; the update view
+// (candidate merge scratch) and the gi view (adjacency lists, prefix sums,
+// coin bits) are never live at the same time and share one region.
+struct Lay {
+    u32 mask, keys0, keys1, cnts0, cnts1;
+    u32 tcnt, ncp, ncn, aux, newexcl;                               // update view
+    u32 qbase, wp, nA, nB, aoff, bs, cursor, alist, wbt, coin;      // gi view
+    u32 mt, red, reds, redi, bcast;
+    u32 coin_cap;  // coin bits of the gi view
+    u32 total;     // bytes
+};
+
+__host__ __device__ inline u32 al16(u32 x) { return (x + 15u) & ~15u; }
+
+__host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, int n_e, int coin_words,
+                                      int gi_dense) {
+    const u32 NW = u32(nt / 32);
+    const u32 vc = u32(vcap), mc = u32(mcap);
+    u32 o = 0;
+    L->mask = o;
+    o += al16(vc * 2u * u32(W) * 8u);
+    L->keys0 = o;
+    o += al16(mc * 4u);
+    L->keys1 = o;
+    o += al16(mc * 4u);
+    L->cnts0 = o;
+    o += al16(mc * 2u);
+    L->cnts1 = o;
+    o += al16(mc * 2u);
+    const u32 uni = o;
+    L->tcnt = o;
+    o += al16(mc * 2u);
+    L->ncp = o;
+    o += al16((vc + 1u) * 2u);
+    L->ncn = o;
+    o += al16((vc + 1u) * 2u);
+    L->aux = o;
+    o += al16(mc * 4u);
+    L->newexcl = o;
+    o += al16((vc + 2u) * 4u);
+    const u32 end_upd = o;
+    o = uni;
+    L->qbase = o;
+    o += al16((mc + 1u) * 4u);
+    L->nA = o;
+    o += al16((vc + 1u) * 4u);
+    if (!gi_dense) {  // walk view: prefix sums and per-variable adjacency
+        L->wp = o;
+        o += al16((mc + 1u) * 4u);
+        L->nB = o;
+        o += al16((vc + 1u) * 4u);
+        L->aoff = o;
+        o += al16((vc + 1u) * 4u);
+        L->bs = o;
+        o += al16((vc + 1u) * 4u);
+        L->cursor = o;
+        o += al16((vc + 1u) * 4u);
+        L->alist = o;
+        o += al16(mc * 2u);
+    } else {
+        L->wp = L->nB = L->aoff = L->bs = L->cursor = L->alist = L->nA;
+    }
+    L->wbt = o;
+    o += al16(u32(n_e + 2) * 8u);
+    L->coin = o;
+    L->coin_cap = u32(coin_words) * 32u;
+    o += al16(u32(coin_words) * 4u);
+    o = o > end_upd ? o : end_upd;
+    L->mt = o;
+    o += 312u * 8u;
+    L->red = o;
+    o += al16((NW + 2u) * 8u);
+    L->reds = o;
+    o += al16(NW * 16u);
+    L->redi = o;
+    o += al16(NW * 8u);
+    L->bcast = o;
+    o += 16u;
+    L->total = o;
+    return o;
 }
 
 }  // namespace tcse

@@ -25,6 +25,16 @@
 //    candidate list is updated incrementally and merged in canonical order.
 //  * double arithmetic uses explicit __dadd_rn/__dmul_rn (no FMA contraction),
 //    matching the reference built for baseline x86-64.
+//  * Greedy-Intersections (score_intersections_from, strategies.hpp:136-153)
+//    is a sequential double sum per candidate q over all other candidates.
+//    It is evaluated EXACTLY in O(deg q) instead of O(m): the candidates
+//    between two consecutive neighbours of q contribute integers c-1, and a
+//    run of integer additions to a double is exact except where the running
+//    sum crosses a binade, which is located by binary search in a prefix sum
+//    and rounded once — the same value the reference's loop produces.
+//
+// Shared memory is one dynamic buffer (g_smem) carved per system; every
+// access goes through g_smem + offset so it compiles to LDS/STS.
 #include <cuda_runtime.h>
 
 #include "launch.h"
@@ -32,6 +42,8 @@
 namespace tcse {
 
 #define FULLMASK 0xffffffffu
+
+extern __shared__ __align__(16) unsigned char g_smem[];
 
 // ------------------------------------------------------------------ keys
 
@@ -48,6 +60,8 @@ constexpr u64 kMtUM = 0xffffffff80000000ULL;
 constexpr u64 kMtLM = 0x7fffffffULL;
 constexpr u64 kMtA = 0xb5026f5aa96619e9ULL;
 constexpr u64 kMtF = 6364136223846793005ULL;
+// top bit of the tempered output = parity of these raw state bits
+constexpr u64 kCoinMask = 0x8080000004000200ULL;
 
 __device__ __forceinline__ u64 mt_temper(u64 z) {
     z ^= (z >> 29) & 0x5555555555555555ULL;
@@ -70,15 +84,6 @@ __device__ __forceinline__ u64 splitmix64(u64 x) {
     return x ^ (x >> 31);
 }
 
-__device__ __forceinline__ u64 mix_seed4(u64 a, u64 b, u64 c, u64 d) {
-    u64 h = 0x5851f42d4c957f2dULL;
-    h = splitmix64(h ^ a);
-    h = splitmix64(h ^ b);
-    h = splitmix64(h ^ c);
-    h = splitmix64(h ^ d);
-    return h;
-}
-
 // generate_canonical<double,53>(mt19937_64): double(x) / 2^64, below 1
 __device__ __forceinline__ double canonical(u64 x) {
     double r = __dmul_rn(__ull2double_rn(x), 0x1p-64);
@@ -90,12 +95,20 @@ __device__ __forceinline__ double uniform_real(u64 x, double a, double b) {
     return __dadd_rn(__dmul_rn(canonical(x), __dsub_rn(b, a)), a);
 }
 
-// ------------------------------------------------------ block primitives
+// ---------------------------------------------------------- smem layout
 
-template <int NT>
-struct Red {
-    static constexpr int NW = NT / 32;
-};
+__shared__ Lay lay;
+
+template <typename T>
+__device__ __forceinline__ T* sp(u32 off) {
+    return reinterpret_cast<T*>(g_smem + off);
+}
+
+// ------------------------------------------------------ block primitives
+//
+// Reductions end right after their single read phase; callers alternate
+// between two scratch buffers (St::rsel), so a buffer is reused only after
+// every thread has passed the next primitive's barrier.
 
 __device__ __forceinline__ u32 warp_incl_scan(u32 v, int lane) {
 #pragma unroll
@@ -107,12 +120,15 @@ __device__ __forceinline__ u32 warp_incl_scan(u32 v, int lane) {
     return v;
 }
 
-// exclusive block scan of one u32 per thread; total in *total
 template <int NT>
 __device__ __forceinline__ u32 block_scan(u32 v, u32* red, u32* total) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const u32 inc = warp_incl_scan(v, lane);
+    if (NW == 1) {
+        *total = __shfl_sync(FULLMASK, inc, 31);
+        return inc - v;
+    }
     if (lane == 31)
         red[warp] = inc;
     __syncthreads();
@@ -125,16 +141,16 @@ __device__ __forceinline__ u32 block_scan(u32 v, u32* red, u32* total) {
             red[NW] = wi;
     }
     __syncthreads();
-    const u32 res = red[warp] + inc - v;
     *total = red[NW];
-    __syncthreads();
-    return res;
+    return red[warp] + inc - v;
 }
 
 template <int NT>
 __device__ __forceinline__ u32 block_max(u32 v, u32* red) {
     constexpr int NW = NT / 32;
     v = __reduce_max_sync(FULLMASK, v);
+    if (NW == 1)
+        return v;
     if ((threadIdx.x & 31) == 0)
         red[threadIdx.x >> 5] = v;
     __syncthreads();
@@ -142,7 +158,6 @@ __device__ __forceinline__ u32 block_max(u32 v, u32* red) {
 #pragma unroll
     for (int w = 1; w < NW; ++w)
         r = max(r, red[w]);
-    __syncthreads();
     return r;
 }
 
@@ -150,6 +165,8 @@ template <int NT>
 __device__ __forceinline__ u32 block_sum(u32 v, u32* red) {
     constexpr int NW = NT / 32;
     v = __reduce_add_sync(FULLMASK, v);
+    if (NW == 1)
+        return v;
     if ((threadIdx.x & 31) == 0)
         red[threadIdx.x >> 5] = v;
     __syncthreads();
@@ -157,7 +174,6 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* red) {
 #pragma unroll
     for (int w = 0; w < NW; ++w)
         r += red[w];
-    __syncthreads();
     return r;
 }
 
@@ -174,6 +190,8 @@ __device__ __forceinline__ int block_argmax_double(double s, int idx, double* re
             idx = i2;
         }
     }
+    if (NW == 1)
+        return __shfl_sync(FULLMASK, idx, 0);
     if ((threadIdx.x & 31) == 0) {
         reds[threadIdx.x >> 5] = s;
         redi[threadIdx.x >> 5] = idx;
@@ -187,165 +205,227 @@ __device__ __forceinline__ int block_argmax_double(double s, int idx, double* re
             bs = reds[w];
             bi = redi[w];
         }
-    __syncthreads();
     return bi;
+}
+
+// ------------------------------------------------- cold helpers (no inline)
+
+// mt19937_64 seeding (one thread, any destination)
+__device__ __noinline__ void mt_seed(u64* mt, u64 s) {
+    u64 x = s;
+    mt[0] = x;
+#pragma unroll 1
+    for (u32 i = 1; i < 312; ++i) {
+        x = kMtF * (x ^ (x >> 62)) + i;
+        mt[i] = x;
+    }
+}
+
+// cooperative twist of the 312-word state (block-uniform call)
+template <int NT>
+__device__ __noinline__ void mt_twist() {
+    constexpr int R = (156 + NT - 1) / NT;
+    u64* mt = sp<u64>(lay.mt);
+    const int tid = threadIdx.x;
+    u64 v[R];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < 156)
+            v[r] = mt_mix(mt[i], mt[i + 1], mt[i + 156]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < 156)
+            mt[i] = v[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = 156 + tid + r * NT;
+        if (i < 312)
+            v[r] = mt_mix(mt[i], mt[i == 311 ? 0 : i + 1], mt[i - 156]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = 156 + tid + r * NT;
+        if (i < 312)
+            mt[i] = v[r];
+    }
+    __syncthreads();
+}
+
+struct Slot {
+    int strategy;
+    double alpha, beta, p_greedy;
+    u64 seed;
+};
+
+// assign_strategies (parallel_search.hpp:183-205) for global process p: the
+// first five outputs of mt19937_64(mix_seed{master, salt, iteration, p})
+__device__ __noinline__ void derive_slot(const SysDesc& sd, u64 p, Slot* out) {
+    u64 h = 0x5851f42d4c957f2dULL;
+    h = splitmix64(h ^ sd.master_seed);
+    h = splitmix64(h ^ sd.salt);
+    h = splitmix64(h ^ u64(int64_t(sd.iteration)));
+    h = splitmix64(h ^ p);
+    u64 x = h;
+    const u64 l0 = x;
+    x = kMtF * (x ^ (x >> 62)) + 1;
+    const u64 l1 = x;
+    x = kMtF * (x ^ (x >> 62)) + 2;
+    const u64 l2 = x;
+    x = kMtF * (x ^ (x >> 62)) + 3;
+    const u64 l3 = x;
+    x = kMtF * (x ^ (x >> 62)) + 4;
+    const u64 l4 = x;
+    x = kMtF * (x ^ (x >> 62)) + 5;
+    const u64 l5 = x;
+#pragma unroll 1
+    for (u32 i = 6; i <= 156; ++i)
+        x = kMtF * (x ^ (x >> 62)) + i;
+    const u64 h0 = x;
+    x = kMtF * (x ^ (x >> 62)) + 157;
+    const u64 h1 = x;
+    x = kMtF * (x ^ (x >> 62)) + 158;
+    const u64 h2 = x;
+    x = kMtF * (x ^ (x >> 62)) + 159;
+    const u64 h3 = x;
+    x = kMtF * (x ^ (x >> 62)) + 160;
+    const u64 h4 = x;
+    const u64 o0 = mt_temper(mt_mix(l0, l1, h0));
+    const u64 o1 = mt_temper(mt_mix(l1, l2, h1));
+    const u64 o2 = mt_temper(mt_mix(l2, l3, h2));
+    const u64 o3 = mt_temper(mt_mix(l3, l4, h3));
+    const u64 o4 = mt_temper(mt_mix(l4, l5, h4));
+    out->alpha = uniform_real(o0, 0.0, 0.5);
+    out->beta = uniform_real(o1, 0.5, 1.0);
+    out->p_greedy = uniform_real(o2, 0.5, 1.0);
+    if (sd.forced >= 0) {
+        out->strategy = sd.forced;
+        out->seed = o3;
+    } else if (sd.iteration == 1 && p == 0) {
+        out->strategy = TCSE_GREEDY;
+        out->seed = o3;
+    } else {
+        double target = __dmul_rn(uniform_real(o3, 0.0, 1.0), sd.weight_total);
+        int st = TCSE_GREEDY;
+        for (int k = 0; k < 7; ++k) {
+            target = __dsub_rn(target, sd.weights[k]);
+            if (target < 0.0) {
+                st = k;
+                break;
+            }
+        }
+        out->strategy = st;
+        out->seed = o4;
+    }
+}
+
+// frequency of (a, b, neg), 1-based ids (count_pairs, linear_system.hpp:151-161)
+template <int W>
+__device__ __forceinline__ int count_pair(int a, int b, int neg) {
+    const u64* pa = sp<u64>(lay.mask) + size_t(a - 1) * 2 * W;
+    const u64* pb = sp<u64>(lay.mask) + size_t(b - 1) * 2 * W;
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+        c += neg ? (__popcll(pa[w] & pb[W + w]) + __popcll(pa[W + w] & pb[w]))
+                 : (__popcll(pa[w] & pb[w]) + __popcll(pa[W + w] & pb[W + w]));
+    return c;
+}
+
+// every pair of the state with count >= minc, canonical order (dump mode,
+// base candidate lists)
+template <int W, int NT>
+__device__ __noinline__ int all_pairs(int V, int minc, u32* okeys, u16* ocnts, int cap, int rsel0) {
+    const int tid = threadIdx.x;
+    int n_total = 0, rsel = rsel0;
+    for (int a = 1; a < V; ++a) {
+        const int L = 2 * (V - a);
+        const int E = (L + NT - 1) / NT;
+        const int e0 = min(L, tid * E), e1 = min(L, e0 + E);
+        u32 local = 0;
+        for (int e = e0; e < e1; ++e)
+            local += count_pair<W>(a, a + 1 + (e >> 1), e & 1) >= minc ? 1u : 0u;
+        u32 total;
+        rsel ^= 1;
+        u32 ex = block_scan<NT>(local, sp<u32>(lay.red) + rsel * (NT / 32 + 2), &total);
+        for (int e = e0; e < e1; ++e) {
+            const int b = a + 1 + (e >> 1);
+            const int cc = count_pair<W>(a, b, e & 1);
+            if (cc >= minc) {
+                const int pos = n_total + int(ex);
+                if (pos < cap) {
+                    okeys[pos] = make_key(a, b, e & 1);
+                    ocnts[pos] = u16(cc);
+                }
+                ++ex;
+            }
+        }
+        n_total += int(total);
+    }
+    __syncthreads();
+    return n_total;
+}
+
+// FNV-1a over (i, j, sign, count) of the candidate list (trace, one thread)
+__device__ __noinline__ u64 cand_hash(const u32* keys, const u16* cnts, int m) {
+    u64 h = 0xcbf29ce484222325ULL;
+    for (int t = 0; t < m; ++t) {
+        const u32 kk = keys[t];
+        const int f[4] = {key_i(kk), key_j(kk), key_neg(kk) ? -1 : 1, int(cnts[t])};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 u = u32(f[q]);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                h ^= (u >> (8 * b)) & 0xffu;
+                h *= 0x100000001b3ULL;
+            }
+        }
+    }
+    return h;
 }
 
 // ------------------------------------------------------------- process
 
 template <int W, int NT>
-struct Proc {
+struct St {
     static constexpr int NW = NT / 32;
-    const SysDesc& sd;
-    int lp;  // local process index
-    int tid, lane, warp;
-
-    // shared-memory carve
-    u64* mask;  // [vcap][2W]
-    u32* keys[2];
-    u16* cnts[2];
-    u16* tcnt;
-    u16* ncp;
-    u16* ncn;
-    u32* aux;
-    u32* newexcl;
-    u32* coin;
-    u32* qbase;
-    u32* nvar;
-    double* wd;
-    double* wb;
-    u64* mt;
-    u32* red;
-    double* reds;
-    int* redi;
-
-    // block-uniform state
+    int tid, lane;
     int V;      // variables alive (n_x + n_f)
     int m;      // candidates
     int cur;    // candidate buffer
     int cost;   // total_cost (linear_system.hpp:202-204)
-    int n_rec;  // record entries written (prefix included in search mode)
-    int n_own;  // substitutions selected by this process
     int mti;    // mt19937_64 position (312 = twist pending)
-    u64 wops;   // algorithmic word-intersections (SURVEY.md 8(d) model), thread 0
-    u32 last_coins;  // coins drawn by the last gi selection (sum of deg)
+    int rsel;   // reduction buffer selector
+    u32 last_coins;
 
-    __device__ Proc(const SysDesc& s, int lp_, unsigned char* smem) : sd(s), lp(lp_) {
-        tid = threadIdx.x;
-        lane = tid & 31;
-        warp = tid >> 5;
-        auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-        size_t off = 0;
-        mask = reinterpret_cast<u64*>(smem + off);
-        off += al(size_t(sd.vcap) * 2 * W * 8);
-        keys[0] = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(sd.mcap) * 4);
-        keys[1] = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(sd.mcap) * 4);
-        cnts[0] = reinterpret_cast<u16*>(smem + off);
-        off += al(size_t(sd.mcap) * 2);
-        cnts[1] = reinterpret_cast<u16*>(smem + off);
-        off += al(size_t(sd.mcap) * 2);
-        const size_t uni = off;
-        tcnt = reinterpret_cast<u16*>(smem + off);
-        off += al(size_t(sd.mcap) * 2);
-        ncp = reinterpret_cast<u16*>(smem + off);
-        off += al(size_t(sd.vcap + 1) * 2);
-        ncn = reinterpret_cast<u16*>(smem + off);
-        off += al(size_t(sd.vcap + 1) * 2);
-        aux = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(sd.mcap) * 4);
-        newexcl = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(sd.vcap + 2) * 4);
-        const size_t end_upd = off;
-        off = uni;
-        coin = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(kCoinWords) * 4);
-        qbase = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(sd.mcap + 1) * 4);
-        nvar = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(sd.vcap + 1) * 4);
-        wd = reinterpret_cast<double*>(smem + off);
-        off += al(size_t(sd.mcap) * 8);
-        wb = reinterpret_cast<double*>(smem + off);
-        off += al(size_t(sd.mcap) * 8);
-        off = off > end_upd ? off : end_upd;
-        mt = reinterpret_cast<u64*>(smem + off);
-        off += 312 * 8;
-        red = reinterpret_cast<u32*>(smem + off);
-        off += al(size_t(NW + 2) * 8);
-        reds = reinterpret_cast<double*>(smem + off);
-        off += al(size_t(NW + 2) * 8);
-        redi = reinterpret_cast<int*>(smem + off);
+    __device__ __forceinline__ u32* keys() { return sp<u32>(cur ? lay.keys1 : lay.keys0); }
+    __device__ __forceinline__ u16* cnts() { return sp<u16>(cur ? lay.cnts1 : lay.cnts0); }
+    __device__ __forceinline__ u64* P(int v) { return sp<u64>(lay.mask) + size_t(v) * 2 * W; }
+    __device__ __forceinline__ u64* N(int v) { return sp<u64>(lay.mask) + size_t(v) * 2 * W + W; }
+    __device__ __forceinline__ u32* red() {
+        rsel ^= 1;
+        return sp<u32>(lay.red) + rsel * (NW + 2);
+    }
+    __device__ __forceinline__ int argmax(double s, int idx) {
+        rsel ^= 1;
+        return block_argmax_double<NT>(s, idx, sp<double>(lay.reds) + rsel * NW, sp<int>(lay.redi) + rsel * NW);
     }
 
-    // ---- masks
-    __device__ __forceinline__ u64* P(int v) { return mask + size_t(v) * 2 * W; }
-    __device__ __forceinline__ u64* N(int v) { return mask + size_t(v) * 2 * W + W; }
-
-    // frequency of (a, b, neg) with 1-based ids (count_pairs, linear_system.hpp:151-161)
-    __device__ __forceinline__ int count_pair(int a, int b, int neg) {
-        const u64* pa = P(a - 1);
-        const u64* na = N(a - 1);
-        const u64* pb = P(b - 1);
-        const u64* nb = N(b - 1);
-        int c = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w)
-            c += neg ? (__popcll(pa[w] & nb[w]) + __popcll(na[w] & pb[w]))
-                     : (__popcll(pa[w] & pb[w]) + __popcll(na[w] & nb[w]));
-        return c;
-    }
-
-    // ---- mt19937_64 (block-uniform: every thread walks the same stream)
-    __device__ void seed_rng(u64 s) {  // one thread
-        u64 x = s;
-        mt[0] = x;
-        for (u32 i = 1; i < 312; ++i) {
-            x = kMtF * (x ^ (x >> 62)) + i;
-            mt[i] = x;
-        }
-    }
-
-    __device__ void twist() {
-        constexpr int R = (156 + NT - 1) / NT;
-        u64 v[R];
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int i = tid + r * NT;
-            if (i < 156)
-                v[r] = mt_mix(mt[i], mt[i + 1], mt[i + 156]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int i = tid + r * NT;
-            if (i < 156)
-                mt[i] = v[r];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int i = 156 + tid + r * NT;
-            if (i < 312)
-                v[r] = mt_mix(mt[i], mt[i == 311 ? 0 : i + 1], mt[i - 156]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int i = 156 + tid + r * NT;
-            if (i < 312)
-                mt[i] = v[r];
-        }
-        __syncthreads();
-        mti = 0;
-    }
-
+    // ---- mt19937_64, block-uniform: every thread walks the same stream
     __device__ __forceinline__ u64 draw() {
-        if (mti >= 312)
-            twist();
-        return mt_temper(mt[mti++]);
+        if (mti >= 312) {
+            mt_twist<NT>();
+            mti = 0;
+        }
+        return mt_temper(sp<u64>(lay.mt)[mti++]);
     }
 
     // uniform_int_distribution downscaling: _S_nd<unsigned __int128>
@@ -365,28 +445,31 @@ struct Proc {
         return hi;
     }
 
-    // n coin flips (uniform_int_distribution<int>(0,1) == top bit) into coin[]
+    // n coin flips (uniform_int_distribution<int>(0,1) == top tempered bit)
     __device__ void draw_coins(u32 nbits) {
+        u32* coin = sp<u32>(lay.coin);
         const u32 words = (nbits + 31) >> 5;
         for (u32 w = tid; w < words; w += NT)
             coin[w] = 0u;
         __syncthreads();
         u32 done = 0;
         while (done < nbits) {
-            if (mti >= 312)
-                twist();
+            if (mti >= 312) {
+                mt_twist<NT>();
+                mti = 0;
+            }
             const u32 n = min(u32(312 - mti), nbits - done);
             const u32 n32 = (n + 31) & ~31u;
+            const u64* mt = sp<u64>(lay.mt) + mti;
             for (u32 e = tid; e < n32; e += NT) {
-                const bool valid = e < n;
-                const u32 bit = valid ? u32(mt_temper(mt[mti + e]) >> 63) : 0u;
+                const u32 bit = e < n ? (u32(__popcll(mt[e] & kCoinMask)) & 1u) : 0u;
                 const u32 ball = __ballot_sync(FULLMASK, bit);
                 if (lane == 0 && ball) {
-                    const u32 pos = done + (e - lane);
-                    const u32 wd_ = pos >> 5, sh = pos & 31;
-                    atomicOr(&coin[wd_], ball << sh);
+                    const u32 pos = done + e;
+                    const u32 w0 = pos >> 5, sh = pos & 31;
+                    atomicOr(&coin[w0], ball << sh);
                     if (sh)
-                        atomicOr(&coin[wd_ + 1], ball >> (32 - sh));
+                        atomicOr(&coin[w0 + 1], ball >> (32 - sh));
                 }
             }
             mti += int(n);
@@ -395,44 +478,43 @@ struct Proc {
         __syncthreads();
     }
 
-    // ---- substitution (apply_substitution, linear_system.hpp:167-189)
-    // returns the number of replaced occurrences; 0 leaves the state untouched
+    // ---- substitution (apply_substitution, linear_system.hpp:167-189):
+    // returns the replaced occurrences; 0 leaves the state untouched
     __device__ int apply(u32 q) {
+        u32* bc = sp<u32>(lay.bcast);
         if (tid == 0) {
             const int i = key_i(q) - 1, j = key_j(q) - 1, neg = key_neg(q);
-            const int k = V;
             u64* pi = P(i);
-            u64* ni = N(i);
             u64* pj = P(j);
-            u64* nj = N(j);
+            u64* pk = P(V);
             u64 rp[W], rn[W];
             int c = 0;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                rp[w] = pi[w] & (neg ? nj[w] : pj[w]);
-                rn[w] = ni[w] & (neg ? pj[w] : nj[w]);
+                rp[w] = pi[w] & (neg ? pj[W + w] : pj[w]);
+                rn[w] = pi[W + w] & (neg ? pj[w] : pj[W + w]);
                 c += __popcll(rp[w]) + __popcll(rn[w]);
             }
             if (c > 0) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     pi[w] &= ~rp[w];
-                    ni[w] &= ~rn[w];
+                    pi[W + w] &= ~rn[w];
                     if (!neg) {
                         pj[w] &= ~rp[w];
-                        nj[w] &= ~rn[w];
+                        pj[W + w] &= ~rn[w];
                     } else {
-                        nj[w] &= ~rp[w];
+                        pj[W + w] &= ~rp[w];
                         pj[w] &= ~rn[w];
                     }
-                    P(k)[w] = rp[w];
-                    N(k)[w] = rn[w];
+                    pk[w] = rp[w];
+                    pk[W + w] = rn[w];
                 }
             }
-            red[NW + 1] = u32(c);
+            bc[0] = u32(c);
         }
         __syncthreads();
-        const int c = int(red[NW + 1]);
+        const int c = int(bc[0]);
         if (c > 0) {
             ++V;
             cost -= c - 1;
@@ -444,25 +526,34 @@ struct Proc {
     __device__ void update(u32 q) {
         const int i = key_i(q), j = key_j(q);
         const int k = V;
-        const u32* ok = keys[cur];
-        const u16* oc = cnts[cur];
+        const u32* ok = keys();
+        const u16* oc = cnts();
+        u16* tcnt = sp<u16>(lay.tcnt);
+        u16* ncp = sp<u16>(lay.ncp);
+        u16* ncn = sp<u16>(lay.ncn);
+        u32* aux = sp<u32>(lay.aux);
+        u32* newexcl = sp<u32>(lay.newexcl);
         // (a) recount old candidates touching i or j (their counts only drop)
         for (int t = tid; t < m; t += NT) {
             const u32 kk = ok[t];
             const int a = key_i(kk), b = key_j(kk);
-            tcnt[t] = (a == i || a == j || b == i || b == j) ? u16(count_pair(a, b, key_neg(kk))) : oc[t];
+            tcnt[t] = (a == i || a == j || b == i || b == j) ? u16(count_pair<W>(a, b, key_neg(kk))) : oc[t];
         }
         // (b) the new variable's pairs (x, k, +/-)
         const u64* pk = P(k - 1);
-        const u64* nk = N(k - 1);
+        u64 kp[W], kn[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            kp[w] = pk[w];
+            kn[w] = pk[W + w];
+        }
         for (int x = tid + 1; x < k; x += NT) {
             const u64* px = P(x - 1);
-            const u64* nx = N(x - 1);
             int cp = 0, cn = 0;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                cp += __popcll(px[w] & pk[w]) + __popcll(nx[w] & nk[w]);
-                cn += __popcll(px[w] & nk[w]) + __popcll(nx[w] & pk[w]);
+                cp += __popcll(px[w] & kp[w]) + __popcll(px[W + w] & kn[w]);
+                cn += __popcll(px[w] & kn[w]) + __popcll(px[W + w] & kp[w]);
             }
             ncp[x] = u16(cp);
             ncn[x] = u16(cn);
@@ -483,7 +574,7 @@ struct Proc {
             }
         }
         u32 total;
-        const u32 excl = block_scan<NT>(local, red, &total);
+        const u32 excl = block_scan<NT>(local, red(), &total);
         const u32 n_old = total & 0xffffu, n_new = total >> 16;
         u32 o = excl & 0xffffu, n = excl >> 16;
         for (int e = e0; e < e1; ++e) {
@@ -499,8 +590,8 @@ struct Proc {
             }
         }
         __syncthreads();
-        u32* dk = keys[cur ^ 1];
-        u16* dc = cnts[cur ^ 1];
+        u32* dk = sp<u32>(cur ? lay.keys0 : lay.keys1);
+        u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
         o = excl & 0xffffu;
         n = excl >> 16;
         for (int e = e0; e < e1; ++e) {
@@ -544,25 +635,25 @@ struct Proc {
 
     // greedy_from (61-69): first maximum in canonical order
     __device__ int sel_greedy() {
-        const u16* c = cnts[cur];
+        const u16* c = cnts();
         u32 best = 0;
         for (int t = tid; t < m; t += NT)
             best = max(best, (u32(c[t]) << 16) | (0xffffu - u32(t)));
-        best = block_max<NT>(best, red);
+        best = block_max<NT>(best, red());
         return int(0xffffu - (best & 0xffffu));
     }
 
     // greedy_alternative_from (71-83): uniform over the argmax set
     __device__ int sel_ga() {
-        const u16* c = cnts[cur];
+        const u16* c = cnts();
         u32 mx = 0;
         for (int t = tid; t < m; t += NT)
             mx = max(mx, u32(c[t]));
-        mx = block_max<NT>(mx, red);
+        mx = block_max<NT>(mx, red());
         u32 cnt = 0;
         for (int t = tid; t < m; t += NT)
             cnt += c[t] == mx ? 1u : 0u;
-        cnt = block_sum<NT>(cnt, red);
+        cnt = block_sum<NT>(cnt, red());
         const u32 r = u32(nd(cnt));
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
@@ -570,185 +661,312 @@ struct Proc {
         for (int e = e0; e < e1; ++e)
             local += c[e] == mx ? 1u : 0u;
         u32 total;
-        u32 ex = block_scan<NT>(local, red, &total);
+        u32 ex = block_scan<NT>(local, red(), &total);
+        u32* bc = sp<u32>(lay.bcast);
         for (int e = e0; e < e1; ++e)
             if (c[e] == mx) {
                 if (ex == r)
-                    redi[NW + 1] = e;
+                    bc[1] = u32(e);
                 ++ex;
             }
         __syncthreads();
-        const int pick = redi[NW + 1];
-        __syncthreads();
-        return pick;
+        return int(bc[1]);
     }
 
     // weighted_random_from (85-98): first q with prefix(c - 1) > u * total
     __device__ int sel_wr() {
-        const u16* c = cnts[cur];
+        const u16* c = cnts();
+        u32* bc = sp<u32>(lay.bcast);
         u32 tot = 0;
         for (int t = tid; t < m; t += NT)
             tot += u32(c[t]) - 1u;
-        tot = block_sum<NT>(tot, red);
+        tot = block_sum<NT>(tot, red());
         const double target = __dmul_rn(uniform_real(draw(), 0.0, 1.0), double(tot));
         if (tid == 0)
-            redi[NW + 1] = m - 1;
+            bc[1] = u32(m - 1);
+        __syncthreads();
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
         u32 local = 0;
         for (int e = e0; e < e1; ++e)
             local += u32(c[e]) - 1u;
         u32 total;
-        u32 s = block_scan<NT>(local, red, &total);
+        u32 s = block_scan<NT>(local, red(), &total);
         for (int e = e0; e < e1; ++e) {
             const u32 s1 = s + u32(c[e]) - 1u;
             if (double(s1) > target && double(s) <= target)
-                redi[NW + 1] = e;
+                bc[1] = u32(e);
             s = s1;
         }
         __syncthreads();
-        const int pick = redi[NW + 1];
-        __syncthreads();
-        return pick;
+        return int(bc[1]);
     }
 
-    // select_greedy_random (119-124)
-    __device__ int sel_gr(double p_greedy) {
-        if (uniform_real(draw(), 0.0, 1.0) < p_greedy)
-            return sel_ga();
-        return sel_wr();
-    }
-
-    // select_greedy_intersections (162-176) with score_intersections_from
-    // (136-153): per candidate q, a sequential double sum over all other
-    // candidates in canonical order (disjoint: c-1; intersecting: one coin,
-    // beta*(c-1) on heads), coins drawn in (q, s) order from the stream
-    __device__ int sel_gi(double alpha, double beta) {
-        if (alpha == 0.0)
-            return sel_greedy();  // gain only; no coins are drawn (140-141)
-        const u32* ks = keys[cur];
-        const u16* c = cnts[cur];
-        for (int v = tid; v <= V; v += NT)
-            nvar[v] = 0u;
+    // select_greedy_intersections (162-176), alpha != 0.  Coins are drawn in
+    // (q, s) order; q's score is the reference's sequential double sum,
+    // evaluated in O(deg q) (see the header comment).
+    __device__ int sel_gi(double alpha, double beta, int dense) {
+        const u32* ks = keys();
+        const u16* c = cnts();
+        const int V1 = V + 1;
+        u32* nA = sp<u32>(lay.nA);
+        u32* nB = sp<u32>(lay.nB);
+        u32* qbase = sp<u32>(lay.qbase);
+        double* wbt = sp<double>(lay.wbt);
+        const u32* coin = sp<u32>(lay.coin);
+        for (int v = tid; v < V1; v += NT) {
+            nA[v] = 0u;
+            if (!dense)
+                nB[v] = 0u;
+        }
+        for (int cc = tid; cc <= sd_ne; cc += NT)
+            wbt[cc] = __dmul_rn(beta, double(cc - 1));
         __syncthreads();
-        for (int t = tid; t < m; t += NT) {
-            const u32 kk = ks[t];
-            atomicAdd(&nvar[key_i(kk)], 1u);
-            atomicAdd(&nvar[key_j(kk)], 1u);
-            const double w = double(int(c[t]) - 1);
-            wd[t] = w;
-            wb[t] = __dmul_rn(beta, w);
+        // per-variable candidate counts (dense: total in nA; walk: A = as
+        // second element, B = as first element)
+        if (dense) {
+            for (int t = tid; t < m; t += NT) {
+                const u32 kk = ks[t];
+                atomicAdd(&nA[key_i(kk)], 1u);
+                atomicAdd(&nA[key_j(kk)], 1u);
+            }
+        } else {
+            u32* bs = sp<u32>(lay.bs);
+            for (int t = tid; t < m; t += NT) {
+                const u32 kk = ks[t];
+                const int a = key_i(kk), b = key_j(kk);
+                atomicAdd(&nA[b], 1u);
+                atomicAdd(&nB[a], 1u);
+                if (t == 0 || key_i(ks[t - 1]) != a)
+                    bs[a] = u32(t);
+            }
         }
         __syncthreads();
-        // coins per q = candidates sharing a variable, minus q itself (and
-        // its opposite-sign twin, counted under both variables)
+        if (!dense) {
+            // A-list offsets: scan over variables
+            u32* aoff = sp<u32>(lay.aoff);
+            u32* cursor = sp<u32>(lay.cursor);
+            const int E = (V1 + NT - 1) / NT;
+            const int e0 = min(V1, tid * E), e1 = min(V1, e0 + E);
+            u32 local = 0;
+            for (int e = e0; e < e1; ++e)
+                local += nA[e];
+            u32 total;
+            u32 ex = block_scan<NT>(local, red(), &total);
+            for (int e = e0; e < e1; ++e) {
+                aoff[e] = ex;
+                cursor[e] = ex;
+                ex += nA[e];
+            }
+        }
+        // coins per q = candidates sharing a variable, minus q itself (and its
+        // opposite-sign twin, counted under both variables); w prefix sums
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
-        u32 local = 0;
-        for (int e = e0; e < e1; ++e) {
-            const u32 kk = ks[e];
-            const u32 twin = (e + 1 < m && ks[e + 1] == (kk | 1u) && !(kk & 1u)) ||
-                                     (e > 0 && (kk & 1u) && ks[e - 1] == (kk & ~1u))
-                                 ? 1u
-                                 : 0u;
-            local += nvar[key_i(kk)] + nvar[key_j(kk)] - 2u - twin;
-        }
         u32 D;
-        u32 ex = block_scan<NT>(local, red, &D);
-        for (int e = e0; e < e1; ++e) {
-            const u32 kk = ks[e];
-            const u32 twin = (e + 1 < m && ks[e + 1] == (kk | 1u) && !(kk & 1u)) ||
-                                     (e > 0 && (kk & 1u) && ks[e - 1] == (kk & ~1u))
-                                 ? 1u
-                                 : 0u;
-            qbase[e] = ex;
-            ex += nvar[key_i(kk)] + nvar[key_j(kk)] - 2u - twin;
+        {
+            u32 ld = 0, lw = 0;
+            for (int e = e0; e < e1; ++e) {
+                const u32 kk = ks[e];
+                const u32 twin = (e + 1 < m && ks[e + 1] == (kk | 1u) && !(kk & 1u)) ||
+                                         (e > 0 && (kk & 1u) && ks[e - 1] == (kk & ~1u))
+                                     ? 1u
+                                     : 0u;
+                const int a = key_i(kk), b = key_j(kk);
+                ld += dense ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
+                lw += u32(c[e]) - 1u;
+            }
+            u32 exd = block_scan<NT>(ld, red(), &D);
+            u32 W_ = 0, exw = 0;
+            if (!dense)
+                exw = block_scan<NT>(lw, red(), &W_);
+            u32* wp = sp<u32>(lay.wp);
+            for (int e = e0; e < e1; ++e) {
+                const u32 kk = ks[e];
+                const u32 twin = (e + 1 < m && ks[e + 1] == (kk | 1u) && !(kk & 1u)) ||
+                                         (e > 0 && (kk & 1u) && ks[e - 1] == (kk & ~1u))
+                                     ? 1u
+                                     : 0u;
+                const int a = key_i(kk), b = key_j(kk);
+                qbase[e] = exd;
+                exd += dense ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
+                if (!dense) {
+                    wp[e] = exw;
+                    exw += u32(c[e]) - 1u;
+                }
+            }
+            if (tid == 0) {
+                qbase[m] = D;
+                if (!dense)
+                    wp[m] = W_;
+            }
         }
-        if (tid == 0)
-            qbase[m] = D;
-        last_coins = D;
         __syncthreads();
+        last_coins = D;
         double best_s = -1.0;
         int best_q = 0x7fffffff;
-        constexpr u32 kCap = u32(kCoinWords) * 32u;
-        int q_lo = 0;
-        while (q_lo < m) {
-            const u32 c0 = qbase[q_lo];
-            // largest q_hi in (q_lo, m] with qbase[q_hi] - c0 <= kCap
-            int lo = q_lo + 1, hi = m;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (qbase[mid] - c0 <= kCap)
-                    lo = mid;
-                else
-                    hi = mid - 1;
+        if (!dense && D <= lay.coin_cap) {
+            u32* aoff = sp<u32>(lay.aoff);
+            u32* cursor = sp<u32>(lay.cursor);
+            u32* bs = sp<u32>(lay.bs);
+            u16* alist = sp<u16>(lay.alist);
+            const u32* wp = sp<u32>(lay.wp);
+            // A lists: candidate indices by second element, index order
+            for (int t = tid; t < m; t += NT)
+                alist[atomicAdd(&cursor[key_j(ks[t])], 1u)] = u16(t);
+            __syncthreads();
+            for (int v = tid; v < V1; v += NT) {
+                const int b0 = int(aoff[v]), n = int(nA[v]);
+#pragma unroll 1
+                for (int x = 1; x < n; ++x) {
+                    const u16 t = alist[b0 + x];
+                    int y = x - 1;
+                    while (y >= 0 && alist[b0 + y] > t) {
+                        alist[b0 + y + 1] = alist[b0 + y];
+                        --y;
+                    }
+                    alist[b0 + y + 1] = t;
+                }
             }
-            const int q_hi = lo;
-            draw_coins(qbase[q_hi] - c0);
-            for (int q = q_lo + tid; q < q_hi; q += NT) {
+            draw_coins(D);  // barrier-separated clear, ends with a barrier
+            for (int q = tid; q < m; q += NT) {
                 const u32 kq = ks[q];
                 const int qi = key_i(kq), qj = key_j(kq);
-                u32 ptr = qbase[q] - c0;
-                double fut = 0.0;
-                for (int s = 0; s < m; ++s) {
-                    if (s == q)
-                        continue;
-                    const u32 kk = ks[s];
-                    const int si = key_i(kk), sj = key_j(kk);
-                    const bool inter = (si == qi) | (si == qj) | (sj == qi) | (sj == qj);
-                    double add;
-                    if (inter) {
-                        const u32 bit = (coin[ptr >> 5] >> (ptr & 31u)) & 1u;
+                const int ai = int(aoff[qi]), nai = int(nA[qi]), bi = int(bs[qi]), li = nai + int(nB[qi]);
+                const int aj = int(aoff[qj]), naj = int(nA[qj]), bj = int(bs[qj]), lj = naj + int(nB[qj]);
+                u32 ptr = qbase[q];
+                double f = 0.0;
+                int prev = 0, pi = 0, pj = 0;
+                for (;;) {
+                    const int xi = pi < li ? (pi < nai ? int(alist[ai + pi]) : bi + (pi - nai)) : 0x7fffffff;
+                    const int xj = pj < lj ? (pj < naj ? int(alist[aj + pj]) : bj + (pj - naj)) : 0x7fffffff;
+                    const int s = min(xi, xj);
+                    pi += xi == s;
+                    pj += xj == s;
+                    f = add_run(f, prev, s == 0x7fffffff ? m : s, wp);
+                    if (s == 0x7fffffff)
+                        break;
+                    prev = s + 1;
+                    if (s != q) {
+                        if ((coin[ptr >> 5] >> (ptr & 31u)) & 1u)
+                            f = __dadd_rn(f, wbt[c[s]]);
                         ++ptr;
-                        add = bit ? wb[s] : 0.0;
-                    } else {
-                        add = wd[s];
                     }
-                    fut = __dadd_rn(fut, add);
                 }
-                const double h = __dadd_rn(wd[q], __dmul_rn(alpha, fut));
+                const double h = __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, f));
                 if (h > best_s || best_q == 0x7fffffff) {
                     best_s = h;
                     best_q = q;
                 }
             }
-            __syncthreads();
-            q_lo = q_hi;
+        } else {
+            // the reference loop itself (one candidate per thread), coins in chunks
+            const u32 cap = lay.coin_cap;
+            int q_lo = 0;
+            while (q_lo < m) {
+                const u32 c0 = qbase[q_lo];
+                int lo = q_lo + 1, hi = m;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (qbase[mid] - c0 <= cap)
+                        lo = mid;
+                    else
+                        hi = mid - 1;
+                }
+                const int q_hi = lo;
+                draw_coins(qbase[q_hi] - c0);
+                for (int q = q_lo + tid; q < q_hi; q += NT) {
+                    const u32 kq = ks[q];
+                    const int qi = key_i(kq), qj = key_j(kq);
+                    u32 ptr = qbase[q] - c0;
+                    double fut = 0.0;
+                    for (int s = 0; s < m; ++s) {
+                        if (s == q)
+                            continue;
+                        const u32 kk = ks[s];
+                        const int si = key_i(kk), sj = key_j(kk);
+                        const bool inter = (si == qi) | (si == qj) | (sj == qi) | (sj == qj);
+                        double add;
+                        if (inter) {
+                            const u32 bit = (coin[ptr >> 5] >> (ptr & 31u)) & 1u;
+                            ++ptr;
+                            add = bit ? wbt[c[s]] : 0.0;
+                        } else {
+                            add = double(int(c[s]) - 1);
+                        }
+                        fut = __dadd_rn(fut, add);
+                    }
+                    const double h = __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, fut));
+                    if (h > best_s || best_q == 0x7fffffff) {
+                        best_s = h;
+                        best_q = q;
+                    }
+                }
+                __syncthreads();
+                q_lo = q_hi;
+            }
         }
-        return block_argmax_double<NT>(best_s, best_q, reds, redi);
+        return argmax(best_s, best_q);
     }
 
-    // select_greedy_potential (196-220): (c-1) + alpha * created, where
+    // Sequential double sum f + w_L + ... + w_{R-1} (w_t = c_t - 1 >= 1,
+    // wp = exclusive prefix sums), bit-identical to adding one at a time:
+    // integer additions are exact until the running sum crosses a binade
+    // (sums stay far below 2^53), where exactly one rounding happens.
+    __device__ __forceinline__ double add_run(double f, int L, int R, const u32* wp) {
+        while (L < R) {
+            const u32 tot = wp[R] - wp[L];
+            if (f == trunc(f))
+                return __dadd_rn(f, double(tot));  // integer + integer: exact
+            const long long bits = __double_as_longlong(f);
+            const double top = __longlong_as_double((long long)((((bits >> 52) & 0x7ff) + 1)) << 52);
+            const double gap = __dsub_rn(top, f);  // exact (Sterbenz)
+            if (double(tot) < gap)
+                return __dadd_rn(f, double(tot));  // stays in the binade: exact
+            // first element whose partial sum reaches the binade top
+            const u32 need = wp[L] + u32(ceil(gap));
+            int lo = L + 1, hi = R;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (wp[mid] >= need)
+                    hi = mid;
+                else
+                    lo = mid + 1;
+            }
+            f = __dadd_rn(f, double(wp[lo] - wp[L]));  // the one rounding
+            L = lo;
+        }
+        return f;
+    }
+
+    // select_greedy_potential (196-220), alpha != 0: (c-1) + alpha * created,
     // created = pairs with the trial variable k reaching frequency >= 2
-    // (only pairs with k can newly become substitutable: counts touching
-    // i or j drop, all others are unchanged)
     __device__ int sel_gp(double alpha) {
-        if (alpha == 0.0)
-            return sel_greedy();
-        const u32* ks = keys[cur];
-        const u16* c = cnts[cur];
+        const u32* ks = keys();
+        const u16* c = cnts();
         double best_s = -1.0;
         int best_q = 0x7fffffff;
         for (int q = tid; q < m; q += NT) {
             const u32 kq = ks[q];
             const int qi = key_i(kq), qj = key_j(kq), neg = key_neg(kq);
+            const u64* a = P(qi - 1);
+            const u64* b = P(qj - 1);
             u64 rp[W], rn[W];
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                rp[w] = P(qi - 1)[w] & (neg ? N(qj - 1)[w] : P(qj - 1)[w]);
-                rn[w] = N(qi - 1)[w] & (neg ? P(qj - 1)[w] : N(qj - 1)[w]);
+                rp[w] = a[w] & (neg ? b[W + w] : b[w]);
+                rn[w] = a[W + w] & (neg ? b[w] : b[W + w]);
             }
             int created = 0;
             for (int x = 1; x <= V; ++x) {
                 if (x == qi || x == qj)
                     continue;
                 const u64* px = P(x - 1);
-                const u64* nx = N(x - 1);
                 int cp = 0, cn = 0;
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
-                    cp += __popcll(px[w] & rp[w]) + __popcll(nx[w] & rn[w]);
-                    cn += __popcll(px[w] & rn[w]) + __popcll(nx[w] & rp[w]);
+                    cp += __popcll(px[w] & rp[w]) + __popcll(px[W + w] & rn[w]);
+                    cn += __popcll(px[w] & rn[w]) + __popcll(px[W + w] & rp[w]);
                 }
                 created += (cp >= 2) + (cn >= 2);
             }
@@ -758,7 +976,7 @@ struct Proc {
                 best_q = q;
             }
         }
-        return block_argmax_double<NT>(best_s, best_q, reds, redi);
+        return argmax(best_s, best_q);
     }
 
     // pick_mixed_substrategy (236-258); weights validated on the host
@@ -773,69 +991,25 @@ struct Proc {
             }
             total = __dadd_rn(total, mix[k]);
         }
-        const int subs[4] = {TCSE_GREEDY_INTERSECTIONS, TCSE_GREEDY_ALTERNATIVE, TCSE_GREEDY_RANDOM,
-                             TCSE_WEIGHTED_RANDOM};
-        if (positive == 1)
-            return subs[only];
-        double target = __dmul_rn(uniform_real(draw(), 0.0, 1.0), total);
+        int pick = 3;
+        if (positive == 1) {
+            pick = only;
+        } else {
+            double target = __dmul_rn(uniform_real(draw(), 0.0, 1.0), total);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            target = __dsub_rn(target, mix[k]);
-            if (target < 0.0)
-                return subs[k];
-        }
-        return subs[3];
-    }
-
-    __device__ u64 cand_hash() {  // one thread: FNV-1a over (i, j, sign, count)
-        u64 h = 0xcbf29ce484222325ULL;
-        auto feed = [&](int v) {
-            const u32 u = u32(v);
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                h ^= (u >> (8 * b)) & 0xffu;
-                h *= 0x100000001b3ULL;
-            }
-        };
-        for (int t = 0; t < m; ++t) {
-            const u32 kk = keys[cur][t];
-            feed(key_i(kk));
-            feed(key_j(kk));
-            feed(key_neg(kk) ? -1 : 1);
-            feed(int(cnts[cur][t]));
-        }
-        return h;
-    }
-
-    // every pair of the current state with count >= minc, canonical order
-    __device__ int all_pairs(int minc, u32* okeys, u16* ocnts, int cap) {
-        int n_total = 0;
-        for (int a = 1; a < V; ++a) {
-            const int L = 2 * (V - a);
-            const int E = (L + NT - 1) / NT;
-            const int e0 = min(L, tid * E), e1 = min(L, e0 + E);
-            u32 local = 0;
-            for (int e = e0; e < e1; ++e)
-                local += count_pair(a, a + 1 + (e >> 1), e & 1) >= minc ? 1u : 0u;
-            u32 total;
-            u32 ex = block_scan<NT>(local, red, &total);
-            for (int e = e0; e < e1; ++e) {
-                const int b = a + 1 + (e >> 1);
-                const int cc = count_pair(a, b, e & 1);
-                if (cc >= minc) {
-                    const int pos = n_total + int(ex);
-                    if (pos < cap) {
-                        okeys[pos] = make_key(a, b, e & 1);
-                        ocnts[pos] = u16(cc);
-                    }
-                    ++ex;
+            for (int k = 0; k < 4; ++k) {
+                target = __dsub_rn(target, mix[k]);
+                if (target < 0.0) {
+                    pick = k;
+                    break;
                 }
             }
-            n_total += int(total);
         }
-        __syncthreads();
-        return n_total;
+        return pick == 0 ? TCSE_GREEDY_INTERSECTIONS
+                         : (pick == 1 ? TCSE_GREEDY_ALTERNATIVE : (pick == 2 ? TCSE_GREEDY_RANDOM : TCSE_WEIGHTED_RANDOM));
     }
+
+    int sd_ne;
 };
 
 __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) {
@@ -843,9 +1017,15 @@ __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) 
         *sd.err_pos = pos;
 }
 
+// Register cap: resident processes per SM are bounded by registers before
+// shared memory unless the kernel is held to ~64 registers at 128 threads.
+template <int NT>
+struct MinBlocks {
+    static constexpr int value = NT == 32 ? 32 : (NT == 64 ? 16 : (NT == 128 ? 8 : 4));
+};
+
 template <int W, int NT>
-__global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ LaunchDesc L) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const __grid_constant__ LaunchDesc L) {
     int s = 0;
 #pragma unroll
     for (int t = 1; t < kMaxSys; ++t)
@@ -855,126 +1035,55 @@ __global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ Laun
     const int lp = int(blockIdx.x) - sd.block_begin;
     if (lp >= sd.n_local)
         return;
-
-    Proc<W, NT> pr(sd, lp, smem);
     const int tid = threadIdx.x;
-    constexpr int NW = NT / 32;
 
-    // ---- process configuration (thread 0) + base state (all threads)
-    __shared__ double s_cfg[4 + 4];
-    __shared__ u64 s_seed;
-    __shared__ int s_int[4];
+    // ---- process configuration (prep_kernel) + base state (all threads)
+    __shared__ SlotRec s_slot;
     if (tid == 0) {
-        int strategy;
-        double alpha, beta, pg;
-        u64 seed;
-        double mix[4];
-        if (sd.mode == kModeSearch) {
-            // assign_strategies (parallel_search.hpp:183-205): first five
-            // outputs of mt19937_64(mix_seed{master, salt, iteration, p})
-            const u64 p = u64(sd.p0 + lp);
-            const u64 ss = mix_seed4(sd.master_seed, sd.salt, u64(int64_t(sd.iteration)), p);
-            u64 lo_[7], hi_[6];
-            u64 x = ss;
-            lo_[0] = x;
-            for (u32 i = 1; i <= 161; ++i) {
-                x = kMtF * (x ^ (x >> 62)) + i;
-                if (i <= 6)
-                    lo_[i] = x;
-                if (i >= 156)
-                    hi_[i - 156] = x;
-            }
-            u64 out[5];
-#pragma unroll
-            for (int t = 0; t < 5; ++t)
-                out[t] = mt_temper(mt_mix(lo_[t], lo_[t + 1], hi_[t]));
-            alpha = uniform_real(out[0], 0.0, 0.5);
-            beta = uniform_real(out[1], 0.5, 1.0);
-            pg = uniform_real(out[2], 0.5, 1.0);
-            int used = 3;
-            if (sd.forced >= 0) {
-                strategy = sd.forced;
-            } else if (sd.iteration == 1 && p == 0) {
-                strategy = TCSE_GREEDY;
-            } else {
-                double target = __dmul_rn(uniform_real(out[3], 0.0, 1.0), sd.weight_total);
-                strategy = TCSE_GREEDY;
-                for (int k = 0; k < 7; ++k) {
-                    target = __dsub_rn(target, sd.weights[k]);
-                    if (target < 0.0) {
-                        strategy = k;
-                        break;
-                    }
-                }
-                used = 4;
-            }
-            seed = out[used];
-            for (int k = 0; k < 4; ++k)
-                mix[k] = sd.mix[k];
-        } else if (sd.mode == kModeRun) {
-            const tcse_process_config& c = sd.cfgs[lp];
-            strategy = c.strategy;
-            alpha = c.alpha;
-            beta = c.beta;
-            pg = c.p_greedy;
-            seed = c.seed;
-            for (int k = 0; k < 4; ++k)
-                mix[k] = c.mix_weights[k];
-        } else {
-            strategy = TCSE_GREEDY;
-            alpha = beta = pg = 0.0;
-            seed = 0;
-            for (int k = 0; k < 4; ++k)
-                mix[k] = 0.0;
-        }
-        const int reinit = (sd.mode == kModeSearch && sd.reinit && sd.reinit[lp]) ? 1 : 0;
-        const bool rng = reinit || strategy == TCSE_GREEDY_ALTERNATIVE || strategy == TCSE_WEIGHTED_RANDOM ||
-                         strategy == TCSE_GREEDY_RANDOM || strategy == TCSE_MIXED ||
-                         (strategy == TCSE_GREEDY_INTERSECTIONS && alpha != 0.0);
-        s_int[0] = strategy;
-        s_int[1] = reinit;
-        s_int[2] = rng ? 1 : 0;
-        s_cfg[0] = alpha;
-        s_cfg[1] = beta;
-        s_cfg[2] = pg;
-        for (int k = 0; k < 4; ++k)
-            s_cfg[4 + k] = mix[k];
-        s_seed = seed;
-        if (rng)
-            pr.seed_rng(seed);
+        carve(&lay, W, NT, sd.vcap, sd.mcap, sd.n_e, sd.coin_words, sd.gi_dense);
+        s_slot = L.slots[blockIdx.x];
     }
+    __syncthreads();
     {
-        const size_t nw = size_t(sd.n_x) * 2 * W;
-        for (size_t t = tid; t < nw; t += NT)
-            pr.mask[t] = sd.base_masks[t];
+        u64* mask = sp<u64>(lay.mask);
+        const int nw = sd.n_x * 2 * W;
+        for (int t = tid; t < nw; t += NT)
+            mask[t] = sd.base_masks[t];
         if (sd.base_keys) {
+            u32* k0 = sp<u32>(lay.keys0);
+            u16* c0 = sp<u16>(lay.cnts0);
             for (int t = tid; t < sd.base_m; t += NT) {
-                pr.keys[0][t] = sd.base_keys[t];
-                pr.cnts[0][t] = sd.base_cnts[t];
+                k0[t] = sd.base_keys[t];
+                c0[t] = sd.base_cnts[t];
             }
+        }
+        if (s_slot.rng) {
+            u64* mt = sp<u64>(lay.mt);
+            const u64* src = L.rng + size_t(blockIdx.x) * 312;
+            for (int t = tid; t < 312; t += NT)
+                mt[t] = src[t];
         }
     }
     __syncthreads();
-    const int strategy = s_int[0];
-    const int reinit = s_int[1];
-    const double alpha = s_cfg[0], beta = s_cfg[1], p_greedy = s_cfg[2];
-    double mix[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        mix[k] = s_cfg[4 + k];
-    const u64 seed = s_seed;
+    const int strategy = s_slot.strategy;
+    const int reinit = s_slot.reinit;
+    const double alpha = s_slot.alpha, beta = s_slot.beta, p_greedy = s_slot.p_greedy;
+    const double* s_mix = s_slot.mix;
+
+    St<W, NT> pr;
+    pr.tid = tid;
+    pr.lane = tid & 31;
     pr.V = sd.n_x;
     pr.cur = 0;
     pr.cost = sd.naive;
-    pr.n_rec = 0;
-    pr.n_own = 0;
     pr.mti = 312;
-    pr.wops = 0;
+    pr.rsel = 0;
     pr.last_coins = 0;
+    pr.sd_ne = sd.n_e;
     if (sd.base_keys) {
         pr.m = sd.base_m;
     } else {
-        pr.m = pr.all_pairs(2, pr.keys[0], pr.cnts[0], sd.mcap);
+        pr.m = all_pairs<W, NT>(pr.V, 2, sp<u32>(lay.keys0), sp<u16>(lay.cnts0), sd.mcap, 0);
         if (pr.m > sd.mcap) {
             set_error(sd, TCSE_ECAPACITY, pr.m);
             return;
@@ -982,7 +1091,8 @@ __global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ Laun
     }
 
     // ---- prefix: reinit from the incumbent (parallel_search.hpp:242-248) or a
-    // fixed replay (cse_engine.hpp:47-57)
+    // fixed replay (cse_engine.hpp:47-57); replayed through the same
+    // apply/update path as the selected substitutions
     const u32* pre = nullptr;
     int n_pre = 0;
     if (reinit) {
@@ -993,94 +1103,170 @@ __global__ void __launch_bounds__(NT) search_kernel(const __grid_constant__ Laun
         n_pre = sd.prefix_len;
         pre = sd.prefix;
     }
+    const bool rec_prefix = reinit != 0;  // records carry the prefix in search mode
     u32* rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
-    for (int t = 0; t < n_pre; ++t) {
-        const u32 q = pre[t];
-        const int qi = key_i(q), qj = key_j(q);
-        if (qi < 1 || qj <= qi || qj > pr.V || pr.apply(q) == 0) {
-            set_error(sd, TCSE_EREPLAY, t);
+    u64* trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
+    const bool dump = sd.mode == kModeDump;
+    int t_pre = 0, n_rec = 0, n_own = 0, step = 0;
+    u64 wops = 0;
+    for (;;) {
+        u32 q;
+        const bool replay = t_pre < n_pre;
+        if (replay) {
+            q = pre[t_pre];
+            const int qi = key_i(q), qj = key_j(q);
+            if (qi < 1 || qj <= qi || qj > pr.V) {
+                set_error(sd, TCSE_EREPLAY, t_pre);
+                if (tid == 0 && sd.out_cost)
+                    sd.out_cost[lp] = -1;
+                return;
+            }
+        } else {
+            if (dump)
+                break;
+            if (trace && tid == 0 && step < sd.trace_stride)
+                trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
+            ++step;
+            if (pr.m == 0)
+                break;
+            int strat = strategy;
+            if (strat == TCSE_MIXED)
+                strat = pr.mixed_sub(s_mix);  // select_mixed (strategies.hpp:260-269)
+            if (strat == TCSE_GREEDY_RANDOM)  // select_greedy_random (119-124)
+                strat = uniform_real(pr.draw(), 0.0, 1.0) < p_greedy ? TCSE_GREEDY_ALTERNATIVE : TCSE_WEIGHTED_RANDOM;
+            if ((strat == TCSE_GREEDY_INTERSECTIONS || strat == TCSE_GREEDY_POTENTIAL) && alpha == 0.0)
+                strat = TCSE_GREEDY;  // gain only (strategies.hpp:140-141, 205-206)
+            const u64 Vt = u64(pr.V), mt_ = u64(pr.m), we = u64(sd.words);
+            int pick;
+            u64 sel = mt_;
+            if (strat == TCSE_GREEDY) {
+                pick = pr.sel_greedy();
+            } else if (strat == TCSE_GREEDY_ALTERNATIVE) {
+                pick = pr.sel_ga();
+            } else if (strat == TCSE_WEIGHTED_RANDOM) {
+                pick = pr.sel_wr();
+            } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
+                pick = pr.sel_gi(alpha, beta, sd.gi_dense);
+                sel += pr.last_coins;
+            } else {
+                pick = pr.sel_gp(alpha);
+                sel += mt_ * (Vt - 2) * 4 * we;
+            }
+            // SURVEY.md 8(d): recount 12(V-1)W_E + substitution 8 W_E + selection
+            wops += 12 * (Vt - 1) * we + 8 * we + sel;
+            q = pr.keys()[pick];
+        }
+        const int c = pr.apply(q);
+        if (c == 0) {  // only a replayed pair can be absent
+            set_error(sd, TCSE_EREPLAY, t_pre);
             if (tid == 0 && sd.out_cost)
                 sd.out_cost[lp] = -1;
             return;
         }
         pr.update(q);
-    }
-    if (reinit) {
-        for (int t = tid; t < n_pre; t += NT)
-            rec[t] = pre[t];
-        pr.n_rec = n_pre;
+        if (replay) {
+            ++t_pre;
+            if (!rec_prefix)
+                continue;
+        } else {
+            ++n_own;
+        }
+        if (tid == 0 && n_rec < sd.sub_cap)
+            rec[n_rec] = q;
+        ++n_rec;
+        if (n_rec > sd.sub_cap) {
+            set_error(sd, TCSE_ECAPACITY, n_rec);
+            return;
+        }
     }
 
-    if (sd.mode == kModeDump) {
+    if (dump) {
         if (sd.dump_min_count >= 2) {
+            const u32* ks = pr.keys();
+            const u16* cs = pr.cnts();
             for (int t = tid; t < pr.m && t < sd.dump_cap; t += NT) {
-                sd.dump_keys[t] = pr.keys[pr.cur][t];
-                sd.dump_cnts[t] = pr.cnts[pr.cur][t];
+                sd.dump_keys[t] = ks[t];
+                sd.dump_cnts[t] = cs[t];
             }
             if (tid == 0)
                 *sd.dump_n = pr.m;
         } else {
-            const int n = pr.all_pairs(sd.dump_min_count, sd.dump_keys, sd.dump_cnts, sd.dump_cap);
+            const int n = all_pairs<W, NT>(pr.V, sd.dump_min_count, sd.dump_keys, sd.dump_cnts, sd.dump_cap,
+                                           pr.rsel);
             if (tid == 0)
                 *sd.dump_n = n;
         }
         return;
     }
-
-    // ---- run_cse main loop (cse_engine.hpp:33-40)
-    u64* trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
-    for (int step = 0;; ++step) {
-        if (trace && tid == 0 && step < sd.trace_stride)
-            trace[step] = pr.cand_hash();
-        if (pr.m == 0)
-            break;
-        int pick;
-        int strat = strategy;
-        if (strat == TCSE_MIXED)
-            strat = pr.mixed_sub(mix);  // select_mixed (strategies.hpp:260-269)
-        switch (strat) {
-            case TCSE_GREEDY: pick = pr.sel_greedy(); break;
-            case TCSE_GREEDY_ALTERNATIVE: pick = pr.sel_ga(); break;
-            case TCSE_WEIGHTED_RANDOM: pick = pr.sel_wr(); break;
-            case TCSE_GREEDY_RANDOM: pick = pr.sel_gr(p_greedy); break;
-            case TCSE_GREEDY_INTERSECTIONS: pick = pr.sel_gi(alpha, beta); break;
-            default: pick = pr.sel_gp(alpha); break;
-        }
-        const u32 q = pr.keys[pr.cur][pick];
-        {
-            // SURVEY.md 8(d): recount 12(V-1)W_E + substitution 8 W_E + selection
-            // (m for g/ga/wr/gr; m + sum deg for gi; m (V-2) 4 W_E for gp)
-            const u64 Vt = u64(pr.V), mt_ = u64(pr.m), we = u64(sd.words);
-            u64 sel = mt_;
-            if (strat == TCSE_GREEDY_INTERSECTIONS && alpha != 0.0)
-                sel += pr.last_coins;
-            if (strat == TCSE_GREEDY_POTENTIAL && alpha != 0.0)
-                sel += mt_ * (Vt - 2) * 4 * we;
-            pr.wops += 12 * (Vt - 1) * we + 8 * we + sel;
-        }
-        pr.apply(q);
-        pr.update(q);
-        if (tid == 0) {
-            if (pr.n_rec < sd.sub_cap)
-                rec[pr.n_rec] = q;
-        }
-        ++pr.n_rec;
-        ++pr.n_own;
-        if (pr.n_rec > sd.sub_cap) {
-            set_error(sd, TCSE_ECAPACITY, pr.n_rec);
-            return;
-        }
-    }
     if (tid == 0) {
         sd.out_cost[lp] = pr.cost;
-        sd.out_len[lp] = pr.n_rec;
-        sd.out_own[lp] = pr.n_own;
+        sd.out_len[lp] = n_rec;
+        sd.out_own[lp] = n_own;
         sd.out_strategy[lp] = strategy;
-        sd.out_seed[lp] = seed;
+        sd.out_seed[lp] = s_slot.seed;
         if (sd.out_wops)
-            sd.out_wops[lp] = pr.wops;
+            sd.out_wops[lp] = wops;
     }
-    (void)NW;
+}
+
+// ------------------------------------------------------------------ K0
+
+// One thread per process: assign_strategies' slot (parallel_search.hpp:
+// 183-205) or the explicit ProcessConfig, the reinit flag, and — when the
+// process will draw — its seeded mt19937_64 state (the 311-step sequential
+// seeding runs here with full-GPU parallelism instead of serially at the
+// start of every search block).
+__global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ LaunchDesc L) {
+    const int b = int(blockIdx.x * blockDim.x + threadIdx.x);
+    if (b >= L.total_blocks)
+        return;
+    int s = 0;
+#pragma unroll
+    for (int t = 1; t < kMaxSys; ++t)
+        if (t < L.nsys && b >= L.sys[t].block_begin)
+            s = t;
+    const SysDesc& sd = L.sys[s];
+    const int lp = b - sd.block_begin;
+    if (lp >= sd.n_local)
+        return;
+    SlotRec r;
+    Slot sl;
+    if (sd.mode == kModeSearch) {
+        derive_slot(sd, u64(sd.p0 + lp), &sl);
+        for (int k = 0; k < 4; ++k)
+            r.mix[k] = sd.mix[k];
+    } else if (sd.mode == kModeRun) {
+        const tcse_process_config& c = sd.cfgs[lp];
+        sl.strategy = c.strategy;
+        sl.alpha = c.alpha;
+        sl.beta = c.beta;
+        sl.p_greedy = c.p_greedy;
+        sl.seed = c.seed;
+        for (int k = 0; k < 4; ++k)
+            r.mix[k] = c.mix_weights[k];
+    } else {
+        sl.strategy = TCSE_GREEDY;
+        sl.alpha = sl.beta = sl.p_greedy = 0.0;
+        sl.seed = 0;
+        for (int k = 0; k < 4; ++k)
+            r.mix[k] = 0.0;
+    }
+    const int reinit = (sd.mode == kModeSearch && sd.reinit && sd.reinit[lp]) ? 1 : 0;
+    const int st = sl.strategy;
+    const bool rng = reinit || st == TCSE_GREEDY_ALTERNATIVE || st == TCSE_WEIGHTED_RANDOM ||
+                     st == TCSE_GREEDY_RANDOM || st == TCSE_MIXED ||
+                     (st == TCSE_GREEDY_INTERSECTIONS && sl.alpha != 0.0);
+    r.strategy = st;
+    r.reinit = reinit;
+    r.rng = rng ? 1 : 0;
+    r.pad = 0;
+    r.alpha = sl.alpha;
+    r.beta = sl.beta;
+    r.p_greedy = sl.p_greedy;
+    r.seed = sl.seed;
+    L.slots[b] = r;
+    if (rng)
+        mt_seed(L.rng + size_t(b) * 312, sl.seed);
 }
 
 // ----------------------------------------------------------------- K2
@@ -1251,12 +1437,30 @@ static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess)
+        return e;
     k<<<L.total_blocks, NT, smem, st>>>(L);
     return cudaGetLastError();
 }
 
+cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st);
+
 cudaError_t launch_search(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st) {
-    if (nt == 128) {
+    prep_kernel<<<(L.total_blocks + 127) / 128, 128, 0, st>>>(L);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return e;
+    return launch_search_w(L, W, nt, smem, st);
+}
+
+cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st) {
+    if (nt == 32) {
+        switch (W) {
+            case 1: return launch_w<1, 32>(L, smem, st);
+            default: break;
+        }
+    } else if (nt == 128) {
         switch (W) {
             case 1: return launch_w<1, 128>(L, smem, st);
             case 2: return launch_w<2, 128>(L, smem, st);
