@@ -326,9 +326,9 @@ def main():
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_gops, "unit": "Gword-ops/s",
                      "frac": achieved / peak_gops if peak_gops else None, "traffic": traffic,
                      "peak_source": "in-repo microbenchmark (tcse_microbench_wordops) on this GPU",
-                     "kernel": "search_kernel<W=1,NT=128>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms)},
+                     "kernel": "search_kernel<W=1,NT=64>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms)},
         "clocks": clk,
-        "gpu_launches": int(2 * args.steps),
+        "gpu_launches": int(3 * args.steps),  # prep + search + reduce per iteration
         "substitution_steps": int(steps_all),
         "incumbent_costs": [r.cost for r, _ in results],
     }
