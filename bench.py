@@ -219,25 +219,34 @@ def main():
     import paper_2512_13365_b200 as T
 
     torch.cuda.set_device(local)
-    gloo = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        gloo = dist.new_group(backend="gloo")
-
-    def allgather(data):
-        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
-        out = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(out, t, group=gloo)
-        return [o.numpy().tobytes() for o in out]
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     dev = T.Device(local)
-    dev.set_partition(rank, world, allgather if world > 1 else None)
+    # world > 1: the per-iteration exchange is an NCCL all-gather (NVLink) of
+    # device payloads between tcse_search_step_begin and _end
+    dev.set_partition(rank, world, None)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
+    bufs = {}
+
+    def step(search):
+        """One optimize_system iteration; returns the number of active systems."""
+        if world == 1:
+            return search.step()
+        key = id(search)
+        if key not in bufs:
+            nb = search.payload_bytes()
+            bufs[key] = (torch.empty(nb, dtype=torch.uint8, device="cuda"),
+                         torch.empty(nb * world, dtype=torch.uint8, device="cuda"))
+        send, recv = bufs[key]
+        search.step_begin(send.data_ptr())
+        dist.all_gather_into_tensor(recv, send)
+        return search.step_end(recv.data_ptr())
     _, sys_rows = load_systems(args.workload)
     systems = [T.LinearSystem(nx, rows) for nx, rows in sys_rows]
     n_total = args.processes * world
@@ -246,7 +255,7 @@ def main():
 
     search = T.Search(systems, cfg, [0, 1, 2], device=dev)
     for _ in range(args.warmup):
-        search.step()
+        step(search)
     torch.cuda.synchronize()
     s0 = search.stats()
     clocks = ClockSampler(local)
@@ -260,7 +269,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        search.step()
+        step(search)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -278,10 +287,15 @@ def main():
     if not args.no_e2e:
         barrier()
         torch.cuda.synchronize()
-        st = {}
         t0 = time.perf_counter()
-        T.optimize_systems(systems, T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed,
-                                                   max_iterations=args.steps), [0, 1, 2], device=dev, stats=st)
+        # the public session API: host CSR in (create uploads the systems),
+        # K iterations, host records out
+        s2 = T.Search(systems, T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed,
+                                              max_iterations=args.steps), [0, 1, 2], device=dev)
+        while step(s2) > 0:
+            pass
+        _, st = s2.result()
+        s2.close()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         e2e = {"steps": st["steps"], "secs": e2e_s, "h2d": st["h2d_bytes"], "d2h": st["d2h_bytes"]}
@@ -335,8 +349,8 @@ def main():
     if e2e:
         line["e2e"] = {"value": sm[5].item() / mx[4].item(), "unit": "substitution steps/s",
                        "h2d_bytes_per_step": e2e["h2d"] / args.steps, "d2h_bytes_per_step": e2e["d2h"] / args.steps,
-                       "call": "tcse_optimize_systems (C ABI, host CSR in, host records out), %d iterations"
-                               % args.steps}
+                       "call": "tcse_search_create/step/result (C ABI, host CSR in, host records out), "
+                               "%d iterations" % args.steps}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(args)

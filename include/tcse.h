@@ -176,9 +176,11 @@ void tcse_destroy(tcse_ctx* ctx);
 int tcse_set_stream(tcse_ctx* ctx, void* stream);
 
 /* Process partition across ranks: this rank runs global process ids
- * [floor(p*rank/world) ...) of every iteration; allgather exchanges the
- * per-iteration costs and local best records.  world = 1 (default) needs no
- * allgather.  The result is identical for every world size. */
+ * [floor(n*rank/world), floor(n*(rank+1)/world)) of every iteration; the
+ * per-iteration payloads (costs + local best record) are exchanged either by
+ * the host allgather callback or by a caller-run device collective around
+ * tcse_search_step_begin/end.  world = 1 (default) needs neither.  The
+ * result is identical for every world size. */
 int tcse_set_partition(tcse_ctx* ctx, int32_t rank, int32_t world,
                        tcse_allgather_fn allgather, void* user);
 
@@ -229,6 +231,19 @@ int tcse_search_create(tcse_ctx* ctx, int32_t n_systems, const tcse_system* syst
                        const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb,
                        void* user, tcse_search** out);
 int tcse_search_step(tcse_search* search, int32_t* n_active);
+
+/* The same iteration in two phases around a caller-run collective (world > 1
+ * without an allgather callback, e.g. ncclAllGather / torch.distributed
+ * all_gather_into_tensor over NVLink).  begin launches the iteration on the
+ * context's stream and writes this rank's exchange payload (per-process
+ * costs of its slice + its best record, tcse_search_payload_bytes() bytes)
+ * to send_dev; the caller all-gathers every rank's payload into recv_dev
+ * (world x payload bytes, rank order) ordered after that stream; end runs the
+ * iteration barrier from recv_dev.  NULL buffers = the library's own (world
+ * 1, or the host callback). */
+size_t tcse_search_payload_bytes(tcse_search* search);
+int tcse_search_step_begin(tcse_search* search, void* send_dev);
+int tcse_search_step_end(tcse_search* search, const void* recv_dev, int32_t* n_active);
 int tcse_search_result(tcse_search* search, tcse_record* best, int32_t* iterations,
                        tcse_stats* stats);
 void tcse_search_destroy(tcse_search* search);

@@ -691,6 +691,40 @@ int or_run_cse(const tcse_system* sys, const tcse_pair* prefix, int32_t n_prefix
 
 /* ------------------------------------------------------ orchestration */
 
+int or_run_process(const tcse_system* sys, const tcse_process_config* slot, int32_t reinit,
+                   const tcse_pair* incumbent, int32_t inc_len, tcse_record* out, int32_t* own) {
+    osys s;
+    int rc = osys_init(&s, sys);
+    if (rc)
+        return rc;
+    mt64 g;
+    mt_seed(&g, slot->seed);
+    int k = 0;
+    if (reinit) {
+        const uint64_t k_max = (uint64_t)(3 * inc_len / 4);
+        k = (int)mt_uniform_int(&g, 1, k_max);
+        rc = osys_replay(&s, incumbent, k);
+        if (rc) {
+            osys_free(&s);
+            return rc;
+        }
+    }
+    tcse_record rec = *out;
+    rec.subs = out->subs + k;
+    rec.cap = out->cap - k;
+    rc = run_cse_state(&s, slot, &g, &rec, NULL, 0);
+    osys_free(&s);
+    if (rc)
+        return rc;
+    memcpy(out->subs, incumbent, sizeof(tcse_pair) * (size_t)k);
+    out->n_subs = k + rec.n_subs;
+    out->cost = rec.cost;
+    out->strategy = rec.strategy;
+    out->seed = rec.seed;
+    *own = rec.n_subs;
+    return TCSE_OK;
+}
+
 /* validate_config (parallel_search.hpp:117-140), flip mode excluded */
 static int validate_config(const tcse_search_config* cfg) {
     if (cfg->n_processes < 0)

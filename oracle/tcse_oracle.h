@@ -50,6 +50,13 @@ int or_run_cse(const tcse_system* sys, const tcse_pair* prefix, int32_t n_prefix
                const tcse_process_config* cfg, tcse_record* out, uint64_t* trace,
                int32_t trace_cap);
 
+/* one process of an optimize_system iteration (the parallel_for body,
+ * parallel_search.hpp:240-252): rng = mt19937_64(slot->seed); if reinit,
+ * k ~ U[1, 3*len/4] and replay of the incumbent prefix; then run_cse.  out
+ * receives prefix + own substitutions; *own = own substitutions. */
+int or_run_process(const tcse_system* sys, const tcse_process_config* slot, int32_t reinit,
+                   const tcse_pair* incumbent, int32_t inc_len, tcse_record* out, int32_t* own);
+
 /* assign_strategies (parallel_search.hpp:172-208); out[n] */
 int or_assign_strategies(const tcse_search_config* cfg, int32_t iteration, int32_t n,
                          uint64_t salt, tcse_process_config* out);

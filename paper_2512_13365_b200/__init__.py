@@ -88,6 +88,10 @@ def lib():
         L.tcse_search_step.argtypes = [C.c_void_p, P(C.c_int32)]
         L.tcse_search_result.argtypes = [C.c_void_p, P(_abi.Record), P(C.c_int32), P(_abi.Stats)]
         L.tcse_search_destroy.argtypes = [C.c_void_p]
+        L.tcse_search_payload_bytes.argtypes = [C.c_void_p]
+        L.tcse_search_payload_bytes.restype = C.c_size_t
+        L.tcse_search_step_begin.argtypes = [C.c_void_p, C.c_void_p]
+        L.tcse_search_step_end.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32)]
         _lib = L
         return L
 
@@ -332,6 +336,21 @@ class Search:
     def step(self):
         left = C.c_int32()
         _check(lib().tcse_search_step(self._h, C.byref(left)))
+        self.active = left.value
+        return self.active
+
+    def payload_bytes(self):
+        """Bytes of this rank's per-iteration exchange payload."""
+        return lib().tcse_search_payload_bytes(self._h)
+
+    def step_begin(self, send_ptr=None):
+        """Launch the iteration; write the payload to device pointer send_ptr."""
+        _check(lib().tcse_search_step_begin(self._h, C.c_void_p(send_ptr) if send_ptr else None))
+
+    def step_end(self, recv_ptr=None):
+        """Finish the iteration from the gathered payloads at recv_ptr."""
+        left = C.c_int32()
+        _check(lib().tcse_search_step_end(self._h, C.c_void_p(recv_ptr) if recv_ptr else None, C.byref(left)))
         self.active = left.value
         return self.active
 

@@ -33,32 +33,9 @@ cudaError_t launch_search(const LaunchDesc& L, int W, int nt, int smem, cudaStre
 struct ReduceLaunch;
 }  // namespace tcse
 
-// ReduceDesc/ReduceLaunch are defined in search.cu; mirror them here.
 namespace tcse {
-struct ReduceDesc {
-    int32_t n;
-    const int32_t* costs;
-    int32_t rec_base, rec_n;
-    const int32_t* lens;
-    const int32_t* strategies;
-    const u64* seeds;
-    const u32* subs;
-    int32_t stride;
-    const int32_t* own;
-    const int32_t* own_len;
-    const u64* own_wops;
-    int32_t own_n;
-    IncState* inc;
-    u32* inc_keys;
-    u8* reinit_next;
-    double fraction;
-    int32_t hist_n;
-};
-struct ReduceLaunch {
-    int32_t nsys;
-    ReduceDesc r[kMaxSys];
-};
-cudaError_t launch_reduce(const ReduceLaunch& RL, int hist_n, cudaStream_t st);
+cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st);
+cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st);
 }  // namespace tcse
 
 using namespace tcse;
@@ -523,7 +500,7 @@ int tcse_set_stream(tcse_ctx* ctx, void* stream) {
 }
 
 int tcse_set_partition(tcse_ctx* ctx, int32_t rank, int32_t world, tcse_allgather_fn allgather, void* user) {
-    if (!ctx || world < 1 || rank < 0 || rank >= world || (world > 1 && !allgather))
+    if (!ctx || world < 1 || rank < 0 || rank >= world)
         return fail(TCSE_EINVAL, "tcse_set_partition: bad rank %d / world %d", rank, world);
     ctx->rank = rank;
     ctx->world = world;
@@ -705,7 +682,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
 namespace {
 
 struct Pool {
-    DBuf cost, len, own, strat, seed, wops, subs, reinit, inc, inc_keys, gcost, stage;
+    DBuf cost, len, own, strat, seed, wops, subs, reinit, inc, inc_keys;
     int sub_cap = 0;
 };
 
@@ -733,6 +710,15 @@ struct tcse_search {
     bool stopped = false;
     cudaEvent_t es0 = nullptr, es1 = nullptr;
     std::chrono::steady_clock::time_point t0;
+    // exchange payload layout (int32 words): per system [n_max costs | 6 | sub_cap]
+    int n_max = 0, words_total = 0;
+    std::vector<int> sys_off;
+    DBuf send, recv;
+    std::vector<int32_t> hsend, hrecv;
+    std::vector<int> act;  // systems active in the pending iteration
+    int32_t* send_used = nullptr;
+    bool pending = false;
+    std::chrono::steady_clock::time_point tx;
     ~tcse_search() {
         if (es0)
             cudaEventDestroy(es0);
@@ -808,13 +794,17 @@ int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_sys
         CU(P.inc_keys.reserve(4 * size_t(P.sub_cap)));
         CU(cudaMemsetAsync(P.inc.p, 0, sizeof(IncState), ctx->stream));
         CU(cudaMemsetAsync(P.reinit.p, 0, size_t(S->n), ctx->stream));
-        if (world > 1) {
-            CU(P.gcost.reserve(4 * size_t(S->n)));
-            CU(P.stage.reserve(4 * size_t(P.sub_cap) + 64));
-        }
         S->hist_n = std::max(S->hist_n, d.h.naive + 1);
     }
     CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
+    S->n_max = (S->n + world - 1) / world + 1;
+    for (int s = 0; s < n_systems; ++s) {
+        S->sys_off.push_back(S->words_total);
+        S->words_total += S->n_max + 6 + S->pool[size_t(s)].sub_cap;
+    }
+    CU(S->send.reserve(4 * size_t(S->words_total)));
+    if (world > 1)
+        CU(S->recv.reserve(4 * size_t(S->words_total) * size_t(world)));
     for (int k = 0; k < 7; ++k)
         S->weight_total += cfg->strategy_weights[k];
     S->active.assign(size_t(n_systems), 1);
@@ -830,103 +820,51 @@ int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_sys
     return TCSE_OK;
 }
 
-// all-gather this rank's costs and best record; stage the global view
-int exchange(tcse_search* S, int s, ReduceDesc* R) {
-    tcse_ctx* ctx = S->ctx;
+XchgDesc xdesc(tcse_search* S, int s) {
     Pool& P = S->pool[size_t(s)];
-    const int n = S->n, world = ctx->world, n_local = S->n_local, p0 = S->p0;
-    auto part = [&](int r) { return int((long long)n * r / world); };
-    const int n_max = (n + world - 1) / world + 1;
-    const int words = n_max + 6 + P.sub_cap;
-    std::vector<int32_t> send(size_t(words), 0), recv(size_t(words) * size_t(world), 0);
-    std::vector<int32_t> c(size_t(std::max(n_local, 1)));
-    CU(cudaMemcpyAsync(c.data(), P.cost.p, 4 * size_t(n_local), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    int rc = check_err(ctx);
-    if (rc)
-        return rc;
-    int lb = -1;
-    for (int t = 0; t < n_local; ++t) {
-        send[size_t(t)] = c[size_t(t)];
-        if (lb < 0 || c[size_t(t)] < c[size_t(lb)])
-            lb = t;
-    }
-    int32_t* hdr = send.data() + n_max;
-    hdr[0] = lb >= 0 ? 1 : 0;
-    if (lb >= 0) {
-        int32_t len = 0, st = 0;
-        u64 sd64 = 0;
-        CU(cudaMemcpyAsync(&len, P.len.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaMemcpyAsync(&st, P.strat.as<int32_t>() + lb, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaMemcpyAsync(&sd64, P.seed.as<u64>() + lb, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        hdr[1] = p0 + lb;
-        hdr[2] = len;
-        hdr[3] = st;
-        std::memcpy(&hdr[4], &sd64, 8);
-        CU(cudaMemcpyAsync(hdr + 6, P.subs.as<u32>() + size_t(lb) * size_t(P.sub_cap), 4 * size_t(len),
-                           cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-    }
-    if (ctx->allgather(send.data(), recv.data(), send.size() * 4, ctx->ag_user) != 0)
-        return fail(TCSE_ENCCL, "exchange: allgather failed");
-    std::vector<int32_t> gcost((size_t)n);
-    int best_r = -1, best_p = -1, best_c = 0;
-    for (int r = 0; r < world; ++r) {
-        const int32_t* rr = recv.data() + size_t(r) * size_t(words);
-        for (int t = 0; t < part(r + 1) - part(r); ++t)
-            gcost[size_t(part(r) + t)] = rr[t];
-        const int32_t* h = rr + n_max;
-        if (h[0]) {
-            const int bp = h[1], bc = rr[bp - part(r)];
-            if (best_r < 0 || bc < best_c || (bc == best_c && bp < best_p)) {
-                best_r = r;
-                best_p = bp;
-                best_c = bc;
-            }
-        }
-    }
-    if (best_r < 0)
-        return fail(TCSE_ENCCL, "exchange: no rank reported a record");
-    const int32_t* h = recv.data() + size_t(best_r) * size_t(words) + n_max;
-    std::vector<int32_t> stage(size_t(4 + P.sub_cap), 0);
-    stage[0] = h[2];
-    stage[1] = h[3];
-    stage[2] = h[4];
-    stage[3] = h[5];
-    std::memcpy(stage.data() + 4, h + 6, 4 * size_t(h[2]));
-    CU(cudaMemcpyAsync(P.gcost.p, gcost.data(), 4 * size_t(n), cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(P.stage.p, stage.data(), 4 * stage.size(), cudaMemcpyHostToDevice, ctx->stream));
-    S->h2d += 4 * uint64_t(n) + 4 * stage.size();
-    S->d2h += 4 * uint64_t(n_local) + 16 + 4 * uint64_t(h[2]);
-    R->costs = P.gcost.as<int32_t>();
-    R->rec_base = best_p;
-    R->rec_n = 1;
-    R->lens = P.stage.as<int32_t>();
-    R->strategies = P.stage.as<int32_t>() + 1;
-    R->seeds = reinterpret_cast<const u64*>(P.stage.as<int32_t>() + 2);
-    R->subs = P.stage.as<u32>() + 4;
-    return TCSE_OK;
+    XchgDesc X;
+    std::memset(&X, 0, sizeof X);
+    X.n = S->n;
+    X.world = S->ctx->world;
+    X.n_max = S->n_max;
+    X.sys_off = S->sys_off[size_t(s)];
+    X.words_total = S->words_total;
+    X.n_local = S->n_local;
+    X.p0 = S->p0;
+    X.sub_cap = P.sub_cap;
+    X.cost = P.cost.as<int32_t>();
+    X.len = P.len.as<int32_t>();
+    X.own = P.own.as<int32_t>();
+    X.strat = P.strat.as<int32_t>();
+    X.seed = P.seed.as<u64>();
+    X.wops = P.wops.as<u64>();
+    X.subs = P.subs.as<u32>();
+    X.inc = P.inc.as<IncState>();
+    X.inc_keys = P.inc_keys.as<u32>();
+    X.reinit_next = P.reinit.as<u8>();
+    X.fraction = S->cfg.reinit_fraction;
+    X.hist_n = S->hist_n;
+    return X;
 }
 
-int search_step(tcse_search* S, int32_t* n_active) {
+// K0 + K1 for every active system, then this rank's exchange payload (K2a)
+int search_step_begin(tcse_search* S, void* send_ext) {
     tcse_ctx* ctx = S->ctx;
     int rc = TCSE_OK;
-    std::vector<int> act;
+    if (S->pending)
+        return fail(TCSE_EINVAL, "tcse_search_step_begin: previous iteration not finished");
+    S->act.clear();
     for (int s = 0; s < S->n_systems; ++s)
         if (S->active[size_t(s)])
-            act.push_back(s);
-    if (act.empty() || S->stopped) {
-        *n_active = 0;
+            S->act.push_back(s);
+    if (S->act.empty() || S->stopped)
         return TCSE_OK;
-    }
     CU(cudaSetDevice(ctx->device));
     const int iteration = ++S->iteration;
-    // ---- K1: every local process of every active system, one launch
     LaunchDesc L;
     std::memset(&L, 0, sizeof L);
     int blocks = 0;
-    for (int s : act) {
+    for (int s : S->act) {
         const DevSys& d = S->dev[size_t(s)];
         Pool& P = S->pool[size_t(s)];
         SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
@@ -970,56 +908,86 @@ int search_step(tcse_search* S, int32_t* n_active) {
         ++S->launches;
         S->processes += uint64_t(blocks);
     }
-    const auto tx = std::chrono::steady_clock::now();
-    // ---- K2 (+ cross-rank exchange): incumbent pool update, next reinit set
-    ReduceLaunch RL;
-    std::memset(&RL, 0, sizeof RL);
-    for (int s : act) {
-        Pool& P = S->pool[size_t(s)];
-        ReduceDesc R;
-        std::memset(&R, 0, sizeof R);
-        R.n = S->n;
-        R.costs = P.cost.as<int32_t>();
-        R.rec_base = 0;
-        R.rec_n = S->n;
-        R.lens = P.len.as<int32_t>();
-        R.strategies = P.strat.as<int32_t>();
-        R.seeds = P.seed.as<u64>();
-        R.subs = P.subs.as<u32>();
-        R.stride = P.sub_cap;
-        R.own = P.own.as<int32_t>();
-        R.own_len = P.len.as<int32_t>();
-        R.own_wops = P.wops.as<u64>();
-        R.own_n = S->n_local;
-        R.inc = P.inc.as<IncState>();
-        R.inc_keys = P.inc_keys.as<u32>();
-        R.reinit_next = P.reinit.as<u8>();
-        R.fraction = S->cfg.reinit_fraction;
-        R.hist_n = S->hist_n;
-        if (ctx->world > 1 && (rc = exchange(S, s, &R)))
-            return rc;
-        RL.r[RL.nsys++] = R;
+    S->tx = std::chrono::steady_clock::now();
+    int32_t* send = send_ext ? static_cast<int32_t*>(send_ext) : S->send.as<int32_t>();
+    XchgLaunch XL;
+    std::memset(&XL, 0, sizeof XL);
+    for (int s : S->act) {
+        XchgDesc X = xdesc(S, s);
+        X.send = send;
+        XL.x[XL.nsys++] = X;
     }
-    CU(launch_reduce(RL, S->hist_n, ctx->stream));
+    CU(launch_pack(XL, ctx->stream));
+    S->send_used = send;
+    S->pending = true;
+    return TCSE_OK;
+}
+
+// exchange (if any) + K2b + host bookkeeping (patience, on_iteration)
+int search_step_end(tcse_search* S, const void* recv_ext, int32_t* n_active) {
+    tcse_ctx* ctx = S->ctx;
+    int rc = TCSE_OK;
+    if (!S->pending) {
+        int left = 0;
+        for (int s = 0; s < S->n_systems; ++s)
+            left += S->active[size_t(s)];
+        *n_active = S->stopped ? 0 : left;
+        return TCSE_OK;
+    }
+    S->pending = false;
+    CU(cudaSetDevice(ctx->device));
+    const int world = ctx->world;
+    const int32_t* recv = S->send_used;
+    if (world > 1) {
+        if (recv_ext) {
+            recv = static_cast<const int32_t*>(recv_ext);
+        } else {
+            if (!ctx->allgather)
+                return fail(TCSE_ENCCL, "exchange: world %d needs an allgather callback or step_begin/step_end", world);
+            const size_t wt = size_t(S->words_total);
+            S->hsend.resize(wt);
+            S->hrecv.resize(wt * size_t(world));
+            CU(cudaMemcpyAsync(S->hsend.data(), S->send_used, 4 * wt, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            if ((rc = check_err(ctx)))
+                return rc;
+            if (ctx->allgather(S->hsend.data(), S->hrecv.data(), 4 * wt, ctx->ag_user) != 0)
+                return fail(TCSE_ENCCL, "exchange: allgather failed");
+            CU(cudaMemcpyAsync(S->recv.p, S->hrecv.data(), 4 * wt * size_t(world), cudaMemcpyHostToDevice,
+                               ctx->stream));
+            S->d2h += 4 * wt;
+            S->h2d += 4 * wt * uint64_t(world);
+            recv = S->recv.as<int32_t>();
+        }
+    }
+    XchgLaunch XL;
+    std::memset(&XL, 0, sizeof XL);
+    for (int s : S->act) {
+        XchgDesc X = xdesc(S, s);
+        X.recv = recv;
+        XL.x[XL.nsys++] = X;
+    }
+    CU(launch_reduce(XL, S->hist_n, ctx->stream));
     CU(cudaEventRecord(S->es1, ctx->stream));
-    std::vector<IncState> st(act.size());
-    for (size_t a = 0; a < act.size(); ++a)
-        CU(cudaMemcpyAsync(&st[a], S->pool[size_t(act[a])].inc.p, sizeof(IncState), cudaMemcpyDeviceToHost,
+    std::vector<IncState> st(S->act.size());
+    for (size_t a = 0; a < S->act.size(); ++a)
+        CU(cudaMemcpyAsync(&st[a], S->pool[size_t(S->act[a])].inc.p, sizeof(IncState), cudaMemcpyDeviceToHost,
                            ctx->stream));
-    S->d2h += sizeof(IncState) * act.size();
+    S->d2h += sizeof(IncState) * S->act.size();
     CU(cudaStreamSynchronize(ctx->stream));
-    S->exchange_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tx).count();
+    S->exchange_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - S->tx).count();
     rc = check_err(ctx);
     if (rc)
         return rc;
     float ms = 0.f;
-    if (blocks > 0 && cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess)
+    if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess)
         S->kernel_ms += ms;
     if (cudaEventElapsedTime(&ms, S->es0, S->es1) == cudaSuccess)
         S->step_ms += ms;
+    const int iteration = S->iteration;
     // ---- host: patience (parallel_search.hpp:261-270) and on_iteration
-    for (size_t a = 0; a < act.size(); ++a) {
-        const int s = act[a];
+    for (size_t a = 0; a < S->act.size(); ++a) {
+        const int s = S->act[a];
         S->hinc[size_t(s)] = st[a];
         S->iters[size_t(s)] = iteration;
         if (st[a].improved) {
@@ -1060,6 +1028,13 @@ int search_step(tcse_search* S, int32_t* n_active) {
         left += S->active[size_t(s)];
     *n_active = S->stopped ? 0 : left;
     return TCSE_OK;
+}
+
+int search_step(tcse_search* S, int32_t* n_active) {
+    int rc = search_step_begin(S, nullptr);
+    if (rc)
+        return rc;
+    return search_step_end(S, nullptr, n_active);
 }
 
 int search_result(tcse_search* S, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
@@ -1149,6 +1124,20 @@ int tcse_search_result(tcse_search* S, tcse_record* best, int32_t* iterations, t
     if (!S)
         return fail(TCSE_EINVAL, "tcse_search_result: bad argument");
     return search_result(S, best, iterations, stats);
+}
+
+size_t tcse_search_payload_bytes(tcse_search* S) { return S ? 4 * size_t(S->words_total) : 0; }
+
+int tcse_search_step_begin(tcse_search* S, void* send_dev) {
+    if (!S)
+        return fail(TCSE_EINVAL, "tcse_search_step_begin: bad argument");
+    return search_step_begin(S, send_dev);
+}
+
+int tcse_search_step_end(tcse_search* S, const void* recv_dev, int32_t* n_active) {
+    if (!S || !n_active)
+        return fail(TCSE_EINVAL, "tcse_search_step_end: bad argument");
+    return search_step_end(S, recv_dev, n_active);
 }
 
 void tcse_search_destroy(tcse_search* S) {

@@ -123,6 +123,38 @@ struct IncState {
     u64 wops;          // accumulated algorithmic word-ops
 };
 
+// Exchange payload of one rank for one system (int32 words, fixed size):
+//   [0, n_max)            this rank's per-process costs (global ids part(r)..)
+//   n_max + 0             1 if the rank ran at least one process
+//   n_max + 1             global id of the rank's best process (min cost, lowest id)
+//   n_max + 2, 3, 4..5    its record length, strategy, seed (lo, hi)
+//   n_max + 6 ..          its record (u32 pair keys), sub_cap entries
+// With world = 1 the gathered buffer is this payload itself, so one code
+// path serves every world size.
+struct XchgDesc {
+    int32_t n, world, n_max, sys_off, words_total;  // layout (words)
+    int32_t n_local, p0, sub_cap;
+    const int32_t* cost;
+    const int32_t* len;
+    const int32_t* own;
+    const int32_t* strat;
+    const u64* seed;
+    const u64* wops;
+    const u32* subs;
+    int32_t* send;        // this rank's payload (all systems), device
+    const int32_t* recv;  // [world][words_total], device
+    IncState* inc;
+    u32* inc_keys;
+    u8* reinit_next;  // [n]
+    double fraction;
+    int32_t hist_n;
+};
+
+struct XchgLaunch {
+    int32_t nsys;
+    XchgDesc x[kMaxSys];
+};
+
 // Shared-memory carve of one process (block).  Byte offsets; the update view
 // (candidate merge scratch) and the gi view (adjacency lists, prefix sums,
 // coin bits) are never live at the same time and share one region.

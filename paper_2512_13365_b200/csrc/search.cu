@@ -1271,54 +1271,83 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
 
 // ----------------------------------------------------------------- K2
 
-struct ReduceDesc {
-    int32_t n;                // processes (global)
-    const int32_t* costs;     // [n] global order
-    // record source: arrays indexed by (p - rec_base) for p in [rec_base, rec_base + rec_n)
-    int32_t rec_base, rec_n;
-    const int32_t* lens;
-    const int32_t* strategies;
-    const u64* seeds;
-    const u32* subs;
-    int32_t stride;
-    const int32_t* own;      // [own_n] selected-substitution counts of this rank's processes
-    const int32_t* own_len;  // [own_n] their record lengths (prefix included)
-    const u64* own_wops;     // [own_n] algorithmic word-ops
-    int32_t own_n;
-    IncState* inc;
-    u32* inc_keys;
-    u8* reinit_next;  // [n] flags for the next iteration
-    double fraction;
-    int32_t hist_n;  // costs lie in [0, hist_n)
-};
-
-struct ReduceLaunch {
-    int32_t nsys;
-    ReduceDesc r[kMaxSys];
-};
+__device__ __forceinline__ int part_of(int n, int world, int r) { return int((long long)n * r / world); }
 
 constexpr int kRedNT = 1024;
 
-__global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ ReduceLaunch RL) {
+// K2a: this rank's payload (local argmin + record copy), one block per system
+__global__ void __launch_bounds__(kRedNT) pack_kernel(const __grid_constant__ XchgLaunch XL) {
+    const XchgDesc& X = XL.x[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ u64 s_min[32];
+    __shared__ int s_bp;
+    int32_t* out = X.send + X.sys_off;
+    u64 best = ~0ULL;
+    for (int t = tid; t < X.n_local; t += kRedNT) {
+        const int32_t c = X.cost[t];
+        out[t] = c;
+        best = min(best, (u64(u32(c)) << 32) | u64(u32(t)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        best = min(best, __shfl_down_sync(FULLMASK, best, o));
+    if (lane == 0)
+        s_min[warp] = best;
+    __syncthreads();
+    if (tid == 0) {
+        u64 b = s_min[0];
+        for (int w = 1; w < kRedNT / 32; ++w)
+            b = min(b, s_min[w]);
+        int32_t* h = out + X.n_max;
+        const int t = X.n_local > 0 ? int(b & 0xffffffffu) : -1;
+        h[0] = t >= 0 ? 1 : 0;
+        h[1] = t >= 0 ? X.p0 + t : -1;
+        h[2] = t >= 0 ? X.len[t] : 0;
+        h[3] = t >= 0 ? X.strat[t] : 0;
+        const u64 sd = t >= 0 ? X.seed[t] : 0;
+        h[4] = int32_t(u32(sd));
+        h[5] = int32_t(u32(sd >> 32));
+        s_bp = t;
+    }
+    __syncthreads();
+    const int t = s_bp;
+    if (t >= 0) {
+        const int L = X.len[t];
+        int32_t* rec = out + X.n_max + 6;
+        for (int e = tid; e < L; e += kRedNT)
+            rec[e] = int32_t(X.subs[size_t(t) * size_t(X.sub_cap) + size_t(e)]);
+    }
+}
+
+// K2b: the iteration barrier over the gathered payloads
+__global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ XchgLaunch XL) {
     extern __shared__ int hist[];
-    const ReduceDesc& R = RL.r[blockIdx.x];
+    const XchgDesc& X = XL.x[blockIdx.x];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ u64 s_min[32];
     __shared__ u64 s_sum[32];
     __shared__ u64 s_rep[32];
     __shared__ u64 s_wop[32];
     __shared__ u32 s_red[34];
-    __shared__ int s_thr[2];
-    // argmin over (cost, process id) — lowest index wins ties (255-260)
+    __shared__ int s_thr[3];
+    const int n = X.n, world = X.world;
+    auto gcost = [&](int p) -> int {
+        int r = int((long long)p * world / n);  // owner rank guess, corrected below
+        while (r + 1 < world && part_of(n, world, r + 1) <= p)
+            ++r;
+        while (r > 0 && part_of(n, world, r) > p)
+            --r;
+        return X.recv[size_t(r) * size_t(X.words_total) + size_t(X.sys_off) + size_t(p - part_of(n, world, r))];
+    };
+    // argmin over (cost, global process id) — lowest index wins ties (255-260)
     u64 best = ~0ULL;
-    u64 steps = 0;
-    for (int p = tid; p < R.n; p += kRedNT)
-        best = min(best, (u64(u32(R.costs[p])) << 32) | u64(u32(p)));
-    u64 replayed = 0, wops = 0;
-    for (int p = tid; p < R.own_n; p += kRedNT) {
-        steps += u64(R.own[p]);
-        replayed += u64(R.own_len[p] - R.own[p]);
-        wops += R.own_wops[p];
+    for (int p = tid; p < n; p += kRedNT)
+        best = min(best, (u64(u32(gcost(p))) << 32) | u64(u32(p)));
+    u64 steps = 0, replayed = 0, wops = 0;
+    for (int t = tid; t < X.n_local; t += kRedNT) {
+        steps += u64(X.own[t]);
+        replayed += u64(X.len[t] - X.own[t]);
+        wops += X.wops[t];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1333,7 +1362,7 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
         s_rep[warp] = replayed;
         s_wop[warp] = wops;
     }
-    for (int v = tid; v < R.hist_n; v += kRedNT)
+    for (int v = tid; v < X.hist_n; v += kRedNT)
         hist[v] = 0;
     __syncthreads();
     if (tid == 0) {
@@ -1346,7 +1375,11 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
         }
         const int bp = int(b & 0xffffffffu);
         const int bc = int(b >> 32);
-        IncState* inc = R.inc;
+        int rb = 0;  // the rank that owns bp carries its record
+        while (rb + 1 < world && part_of(n, world, rb + 1) <= bp)
+            ++rb;
+        const int32_t* h = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max);
+        IncState* inc = X.inc;
         inc->best_p = bp;
         inc->best_cost = bc;
         inc->steps += st;
@@ -1355,39 +1388,41 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
         if (!inc->have || bc < inc->cost) {  // strictly better (261-266)
             inc->have = 1;
             inc->cost = bc;
-            inc->len = R.lens[bp - R.rec_base];
-            inc->strategy = R.strategies[bp - R.rec_base];
-            inc->seed = R.seeds[bp - R.rec_base];
+            inc->len = h[2];
+            inc->strategy = h[3];
+            inc->seed = u64(u32(h[4])) | (u64(u32(h[5])) << 32);
             inc->improved = 1;
         } else {
             inc->improved = 0;
         }
-        s_thr[0] = inc->improved ? bp : -1;
+        s_thr[0] = inc->improved ? rb : -1;
         s_thr[1] = inc->len;
     }
     __syncthreads();
-    const int bp = s_thr[0];
+    const int rb = s_thr[0];
     const int inc_len = s_thr[1];
-    if (bp >= 0)
+    if (rb >= 0) {
+        const int32_t* rec = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + 6;
         for (int t = tid; t < inc_len; t += kRedNT)
-            R.inc_keys[t] = R.subs[size_t(bp - R.rec_base) * size_t(R.stride) + size_t(t)];
+            X.inc_keys[t] = u32(rec[t]);
+    }
     // pick_reinit (149-163) for the next iteration, only if the incumbent can
     // share a prefix (235-237)
-    long long want = llround(__dmul_rn(R.fraction, double(R.n)));
-    const int count = inc_len >= 2 ? int(min(want, (long long)R.n)) : 0;
+    const long long want = llround(__dmul_rn(X.fraction, double(n)));
+    const int count = inc_len >= 2 ? int(min(want, (long long)n)) : 0;
     if (count <= 0) {
-        for (int p = tid; p < R.n; p += kRedNT)
-            R.reinit_next[p] = 0;
+        for (int p = tid; p < n; p += kRedNT)
+            X.reinit_next[p] = 0;
         return;
     }
-    for (int p = tid; p < R.n; p += kRedNT)
-        atomicAdd(&hist[min(max(R.costs[p], 0), R.hist_n - 1)], 1);
+    for (int p = tid; p < n; p += kRedNT)
+        atomicAdd(&hist[min(max(gcost(p), 0), X.hist_n - 1)], 1);
     __syncthreads();
     if (tid == 0) {
         // threshold cost c*: all costs > c* are chosen, plus the first `need`
         // processes (by index) with cost == c* (stable order, 158-160)
         int acc = 0, cstar = 0, need = 0;
-        for (int c = R.hist_n - 1; c >= 0; --c) {
+        for (int c = X.hist_n - 1; c >= 0; --c) {
             if (acc + hist[c] >= count) {
                 cstar = c;
                 need = count - acc;
@@ -1400,11 +1435,11 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
     }
     __syncthreads();
     const int cstar = s_thr[0], need = s_thr[1];
-    const int E = (R.n + kRedNT - 1) / kRedNT;
-    const int e0 = min(R.n, tid * E), e1 = min(R.n, e0 + E);
+    const int E = (n + kRedNT - 1) / kRedNT;
+    const int e0 = min(n, tid * E), e1 = min(n, e0 + E);
     u32 local = 0;
     for (int e = e0; e < e1; ++e)
-        local += R.costs[e] == cstar ? 1u : 0u;
+        local += gcost(e) == cstar ? 1u : 0u;
     const u32 inc_ = warp_incl_scan(local, lane);
     if (lane == 31)
         s_red[warp] = inc_;
@@ -1417,7 +1452,7 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
     __syncthreads();
     u32 ex = s_red[warp] + inc_ - local;
     for (int e = e0; e < e1; ++e) {
-        const int c = R.costs[e];
+        const int c = gcost(e);
         u8 f = 0;
         if (c > cstar) {
             f = 1;
@@ -1425,7 +1460,7 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
             f = ex < u32(need) ? 1 : 0;
             ++ex;
         }
-        R.reinit_next[e] = f;
+        X.reinit_next[e] = f;
     }
 }
 
@@ -1485,12 +1520,17 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, int smem, cudaSt
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_reduce(const ReduceLaunch& RL, int hist_n, cudaStream_t st) {
+cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st) {
+    pack_kernel<<<XL.nsys, kRedNT, 0, st>>>(XL);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st) {
     const int smem = hist_n * int(sizeof(int));
     cudaError_t e = cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
-    reduce_kernel<<<RL.nsys, kRedNT, smem, st>>>(RL);
+    reduce_kernel<<<XL.nsys, kRedNT, smem, st>>>(XL);
     return cudaGetLastError();
 }
 
