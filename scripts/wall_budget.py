@@ -1,0 +1,83 @@
+"""Best additions at a fixed wall time, reference CPU path vs the B200 search.
+
+For each scheme: the reference optimize_scheme (oracle/_ref, all host cores,
+default config: tier process count, patience 10) runs to convergence; its wall
+time T_ref is the budget.  The GPU search (same weights, reinit, patience,
+seed) runs with the paper's GPU process counts (16384 for
+rank < 100, 8192 below 200, 2048 above) and stops at the first iteration
+barrier after T_ref (an on_iteration abort, as SURVEY.md 8(d) prescribes for
+the reference).  Every GPU record is re-verified (replay + expand_and_verify).
+"""
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2512_13365_b200 as T  # noqa: E402
+from oracle_lib import reference  # noqa: E402
+
+
+def gpu_count(r):
+    return 16384 if r < 100 else (8192 if r < 200 else 2048)
+
+
+def run(name, seed=1):
+    path = os.path.join(ROOT, "tests", "golden", "schemes", name + ".json")
+    text = open(path).read()
+    s = T.parse_scheme(text)
+    ref = reference()
+    cfg = T.SearchConfig(master_seed=seed)
+    buf = C.create_string_buffer(1 << 24)
+    n = C.c_int32()
+    t0 = time.time()
+    rc = ref.ref_optimize_scheme_json(text.encode(), C.byref(cfg.to_c()), os.cpu_count(), buf, len(buf), C.byref(n))
+    t_ref = time.time() - t0
+    assert rc == 0, ref.ref_last_error()
+    rj = json.loads(buf.value.decode())
+    systems = [T.LinearSystem(nx, rows) for nx, rows in T.extract_systems(s)]
+    N = gpu_count(s["r"])
+    gcfg = T.SearchConfig(n_processes=N, master_seed=seed)
+    start = time.time()
+    stopped = {"flag": False}
+
+    def on_it(sys_index, iteration, rec):
+        if time.time() - start >= t_ref:
+            stopped["flag"] = True
+            return True
+        return False
+
+    st = {}
+    res = T.optimize_systems(systems, gcfg, [0, 1, 2], on_iteration=on_it, stats=st)
+    t_gpu = time.time() - start
+    costs = []
+    for sys_, (rec, it) in zip(systems, res):
+        ok, cost = T.verify_record(sys_, rec.substitutions)
+        assert ok and cost == rec.cost
+        costs.append(rec.cost)
+    return {
+        "scheme": name, "digest": T.scheme_digest(s), "shape": "%dx%dx%d:%d" % (s["m"], s["n"], s["p"], s["r"]),
+        "naive": [T.naive_cost(r) for _, r in T.extract_systems(s)],
+        "reference": {"total": rj["total"], "components": [rj["components"][k]["cost"] for k in "uvw"],
+                      "processes": rj["config"]["n_processes"], "iterations": rj["iterations"],
+                      "wall_s": round(t_ref, 3), "threads": os.cpu_count()},
+        "gpu": {"total": sum(costs), "components": costs, "processes": N, "iterations": [it for _, it in res],
+                "wall_s": round(t_gpu, 3), "stopped_at_budget": stopped["flag"], "steps": st["steps"],
+                "steps_per_s_device": st["steps"] / max(1e-9, st["kernel_ms"]) * 1e3},
+        "gpu_le_reference": sum(costs) <= rj["total"],
+    }
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["laderman", "sxs", "sxs_border", "naive555_f1000", "sxl", "naive666_f3000"]
+    rows = []
+    for nm in names:
+        r = run(nm)
+        rows.append(r)
+        print(json.dumps(r), flush=True)
+    out = os.path.join(ROOT, "gpurun_out", "wall_budget.json")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    json.dump(rows, open(out, "w"), indent=1)
