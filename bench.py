@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="payload all-gather transport for --gpus > 1 (gloo stages through host memory; "
+                         "lets the multi-rank path run with several ranks on one GPU for testing)")
     return ap.parse_args()
 
 
@@ -142,7 +145,10 @@ def run_reference(args, rank, world):
         C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]
     threads = os.cpu_count() or 1
     _, systems = load_systems(args.workload)
-    n_proc = args.processes * args.gpus  # the same global process count as the GPU arm
+    # the GPU arm runs processes x gpus per component; the CPU's steps/s does
+    # not depend on the process count once it exceeds the thread count, so the
+    # reference is sampled at up to 16384 processes to bound its run time
+    n_proc = min(args.processes * args.gpus, 16384)
     its = args.warmup + args.steps
     cfg = T.SearchConfig(n_processes=n_proc, patience=1 << 30, master_seed=args.seed, max_iterations=its).to_c()
     secs = steps = 0.0
@@ -167,8 +173,8 @@ def run_reference(args, rank, world):
         "config": config_block(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "substitution steps/s", "cores": threads, "kind": "reference",
                          "sample": "iterations %d..%d of optimize_system on U, V, W (sequential, as "
-                                   "optimize_scheme runs them), %d processes each, threads=%d"
-                                   % (args.warmup + 1, its, n_proc, threads)},
+                                   "optimize_scheme runs them), %d processes each (GPU arm: %d), threads=%d"
+                                   % (args.warmup + 1, its, n_proc, args.processes * args.gpus, threads)},
         "e2e": {"value": value, "unit": "substitution steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "substitution_steps": int(steps),
     }
@@ -218,9 +224,13 @@ def main():
     import torch.distributed as dist
     import paper_2512_13365_b200 as T
 
+    local = local % max(1, torch.cuda.device_count())  # identity with one rank per GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -245,7 +255,13 @@ def main():
                          torch.empty(nb * world, dtype=torch.uint8, device="cuda"))
         send, recv = bufs[key]
         search.step_begin(send.data_ptr())
-        dist.all_gather_into_tensor(recv, send)
+        if args.dist_backend == "nccl":
+            dist.all_gather_into_tensor(recv, send)  # NCCL over NVLink, ordered after the launch stream
+        else:
+            torch.cuda.synchronize()
+            parts = [torch.empty(send.numel(), dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, send.cpu())
+            recv.copy_(torch.cat(parts))
         return search.step_end(recv.data_ptr())
     _, sys_rows = load_systems(args.workload)
     systems = [T.LinearSystem(nx, rows) for nx, rows in sys_rows]
@@ -306,8 +322,9 @@ def main():
     vals = torch.tensor([total_ms, float(steps_local), float(wops), kernel_ms,
                          e2e["secs"] if e2e else 0.0, float(e2e["steps"] if e2e else 0)], dtype=torch.float64)
     if world > 1:
-        mx = vals.clone().cuda()
-        sm = vals.clone().cuda()
+        dev_ = "cuda" if args.dist_backend == "nccl" else "cpu"
+        mx = vals.clone().to(dev_)
+        sm = vals.clone().to(dev_)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         mx, sm = mx.cpu(), sm.cpu()

@@ -29,7 +29,7 @@
 #include "launch.h"
 
 namespace tcse {
-cudaError_t launch_search(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st);
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st);
 struct ReduceLaunch;
 }  // namespace tcse
 
@@ -249,11 +249,20 @@ int gi_dense_for(const HostSys& h) {
     return h.mcap <= 640 ? 1 : 0;
 }
 
+// one gi form per launch: dense only if every system of the launch prefers it
+bool launch_dense(const std::vector<DevSys*>& sys) {
+    bool dense = true;
+    for (auto* d : sys)
+        dense = dense && gi_dense_for(d->h);
+    return dense;
+}
+
 int smem_for(int nt, int W, const std::vector<DevSys*>& sys) {
+    const bool dense = launch_dense(sys);
     u32 mx = 0;
     for (auto* d : sys) {
         Lay L;
-        mx = std::max(mx, carve(&L, W, nt, d->h.vcap, d->h.mcap, d->h.n_e, coin_words_for(d->h), gi_dense_for(d->h)));
+        mx = std::max(mx, carve(&L, W, nt, d->h.vcap, d->h.mcap, d->h.n_e, coin_words_for(d->h), dense));
     }
     return int(mx);
 }
@@ -289,7 +298,7 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.naive = d.h.naive;
     sd.words = d.h.w_need;
     sd.coin_words = coin_words_for(d.h);
-    sd.gi_dense = gi_dense_for(d.h);
+    sd.gi_dense = gi_dense_for(d.h);  // overwritten with the launch's form
     sd.vcap = d.h.vcap;
     sd.mcap = d.h.mcap;
     sd.sub_cap = d.h.naive / 2 + 1;
@@ -328,7 +337,8 @@ int run_dump(tcse_ctx* ctx, DevSys& d, const u32* d_prefix, int n_prefix, int mi
     int prc = attach_prep(ctx, &L);
     if (prc)
         return prc;
-    CU(launch_search(L, d.W, pick_nt(ctx, d.W), smem_for(pick_nt(ctx, d.W), d.W, v), ctx->stream));
+    L.sys[0].gi_dense = launch_dense(v);
+    CU(launch_search(L, d.W, pick_nt(ctx, d.W), launch_dense(v), smem_for(pick_nt(ctx, d.W), d.W, v), ctx->stream));
     int rc = check_err(ctx);
     if (rc)
         return rc;
@@ -631,7 +641,8 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     if (rc)
         return rc;
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
-    CU(launch_search(L, W, pick_nt(ctx, W), smem_for(pick_nt(ctx, W), W, v), ctx->stream));
+    L.sys[0].gi_dense = launch_dense(v);
+    CU(launch_search(L, W, pick_nt(ctx, W), launch_dense(v), smem_for(pick_nt(ctx, W), W, v), ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
     rc = check_err(ctx);
     if (rc)
@@ -697,6 +708,7 @@ struct tcse_search {
     tcse_iter_cb cb = nullptr;
     void* user = nullptr;
     int n = 0, p0 = 0, n_local = 0, Wmax = 1, nt = 128, smem = 0, hist_n = 1;
+    bool dense = true;
     double weight_total = 0.0;
     std::unique_ptr<DevSys[]> dev;
     std::unique_ptr<Pool[]> pool;
@@ -775,6 +787,7 @@ int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_sys
         dptr.push_back(&d);
     }
     S->smem = smem_for(S->nt, S->Wmax, dptr);
+    S->dense = launch_dense(dptr);
     if (S->smem > 227 * 1024 - 1024)
         return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", S->smem);
     for (int s = 0; s < n_systems; ++s) {
@@ -903,7 +916,9 @@ int search_step_begin(tcse_search* S, void* send_ext) {
     CU(cudaEventRecord(S->es0, ctx->stream));
     if (blocks > 0) {
         CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        CU(launch_search(L, S->Wmax, S->nt, S->smem, ctx->stream));
+        for (int t = 0; t < L.nsys; ++t)
+            L.sys[t].gi_dense = S->dense;
+        CU(launch_search(L, S->Wmax, S->nt, S->dense, S->smem, ctx->stream));
         CU(cudaEventRecord(ctx->ev1, ctx->stream));
         ++S->launches;
         S->processes += uint64_t(blocks);

@@ -705,7 +705,8 @@ struct St {
     // select_greedy_intersections (162-176), alpha != 0.  Coins are drawn in
     // (q, s) order; q's score is the reference's sequential double sum,
     // evaluated in O(deg q) (see the header comment).
-    __device__ int sel_gi(double alpha, double beta, int dense) {
+    template <bool dense>
+    __device__ int sel_gi(double alpha, double beta) {
         const u32* ks = keys();
         const u16* c = cnts();
         const int V1 = V + 1;
@@ -860,7 +861,9 @@ struct St {
                 }
             }
         } else {
-            // the reference loop itself (one candidate per thread), coins in chunks
+            // the reference loop itself, coins in chunks; each thread carries
+            // up to K candidates through one pass (K independent double chains)
+            constexpr int K = 3;
             const u32 cap = lay.coin_cap;
             int q_lo = 0;
             while (q_lo < m) {
@@ -875,32 +878,47 @@ struct St {
                 }
                 const int q_hi = lo;
                 draw_coins(qbase[q_hi] - c0);
-                for (int q = q_lo + tid; q < q_hi; q += NT) {
-                    const u32 kq = ks[q];
-                    const int qi = key_i(kq), qj = key_j(kq);
-                    u32 ptr = qbase[q] - c0;
-                    double fut = 0.0;
+                for (int q0 = q_lo + tid; q0 < q_hi; q0 += K * NT) {
+                    int qv[K], qi[K], qj[K];
+                    u32 ptr[K];
+                    double fut[K];
+#pragma unroll
+                    for (int t = 0; t < K; ++t) {
+                        qv[t] = q0 + t * NT;
+                        const bool on = qv[t] < q_hi;
+                        const u32 kq = on ? ks[qv[t]] : 0u;
+                        qi[t] = on ? key_i(kq) : -1;  // -1 never matches a variable
+                        qj[t] = on ? key_j(kq) : -1;
+                        ptr[t] = on ? qbase[qv[t]] - c0 : 0u;
+                        fut[t] = 0.0;
+                    }
                     for (int s = 0; s < m; ++s) {
-                        if (s == q)
-                            continue;
                         const u32 kk = ks[s];
                         const int si = key_i(kk), sj = key_j(kk);
-                        const bool inter = (si == qi) | (si == qj) | (sj == qi) | (sj == qj);
-                        double add;
-                        if (inter) {
-                            const u32 bit = (coin[ptr >> 5] >> (ptr & 31u)) & 1u;
-                            ++ptr;
-                            add = bit ? wbt[c[s]] : 0.0;
-                        } else {
-                            add = double(int(c[s]) - 1);
+                        const u16 cs = c[s];
+                        const double wd = double(int(cs) - 1);
+                        const double wb = wbt[cs];
+#pragma unroll
+                        for (int t = 0; t < K; ++t) {
+                            const bool self = s == qv[t];
+                            const bool inter = !self && ((si == qi[t]) | (si == qj[t]) | (sj == qi[t]) | (sj == qj[t]));
+                            double add = self ? 0.0 : wd;  // q itself is skipped (fut + 0.0 == fut)
+                            if (inter) {
+                                add = ((coin[ptr[t] >> 5] >> (ptr[t] & 31u)) & 1u) ? wb : 0.0;
+                                ++ptr[t];
+                            }
+                            fut[t] = __dadd_rn(fut[t], add);
                         }
-                        fut = __dadd_rn(fut, add);
                     }
-                    const double h = __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, fut));
-                    if (h > best_s || best_q == 0x7fffffff) {
-                        best_s = h;
-                        best_q = q;
-                    }
+#pragma unroll
+                    for (int t = 0; t < K; ++t)
+                        if (qv[t] < q_hi) {
+                            const double h = __dadd_rn(double(int(c[qv[t]]) - 1), __dmul_rn(alpha, fut[t]));
+                            if (h > best_s || best_q == 0x7fffffff) {
+                                best_s = h;
+                                best_q = qv[t];
+                            }
+                        }
                 }
                 __syncthreads();
                 q_lo = q_hi;
@@ -1024,7 +1042,7 @@ struct MinBlocks {
     static constexpr int value = NT == 32 ? 32 : (NT == 64 ? 16 : (NT == 128 ? 8 : 4));
 };
 
-template <int W, int NT>
+template <int W, int NT, bool GID>
 __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const __grid_constant__ LaunchDesc L) {
     int s = 0;
 #pragma unroll
@@ -1146,7 +1164,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             } else if (strat == TCSE_WEIGHTED_RANDOM) {
                 pick = pr.sel_wr();
             } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
-                pick = pr.sel_gi(alpha, beta, sd.gi_dense);
+                pick = pr.template sel_gi<GID>(alpha, beta);
                 sel += pr.last_coins;
             } else {
                 pick = pr.sel_gp(alpha);
@@ -1466,9 +1484,9 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
 
 // ------------------------------------------------------------ dispatch
 
-template <int W, int NT>
+template <int W, int NT, bool GID>
 static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
-    auto k = search_kernel<W, NT>;
+    auto k = search_kernel<W, NT, GID>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
@@ -1479,45 +1497,32 @@ static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st);
+// instantiated (W words, block size, gi form) combinations; the host picks
+// the block size with pick_nt() and the gi form by problem size
+cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
+#define TCSE_CASE(w_, nt_)                                                                      \
+    if (W == w_ && nt == nt_)                                                                   \
+        return dense ? launch_w<w_, nt_, true>(L, smem, st) : launch_w<w_, nt_, false>(L, smem, st);
+    TCSE_CASE(1, 32)
+    TCSE_CASE(1, 64)
+    TCSE_CASE(2, 64)
+    TCSE_CASE(1, 128)
+    TCSE_CASE(2, 128)
+    TCSE_CASE(3, 128)
+    TCSE_CASE(4, 128)
+    TCSE_CASE(8, 128)
+    TCSE_CASE(1, 256)
+    TCSE_CASE(3, 256)
+#undef TCSE_CASE
+    return cudaErrorInvalidValue;
+}
 
-cudaError_t launch_search(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st) {
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
     prep_kernel<<<(L.total_blocks + 127) / 128, 128, 0, st>>>(L);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
-    return launch_search_w(L, W, nt, smem, st);
-}
-
-cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, int smem, cudaStream_t st) {
-    if (nt == 32) {
-        switch (W) {
-            case 1: return launch_w<1, 32>(L, smem, st);
-            default: break;
-        }
-    } else if (nt == 128) {
-        switch (W) {
-            case 1: return launch_w<1, 128>(L, smem, st);
-            case 2: return launch_w<2, 128>(L, smem, st);
-            case 3: return launch_w<3, 128>(L, smem, st);
-            case 4: return launch_w<4, 128>(L, smem, st);
-            case 8: return launch_w<8, 128>(L, smem, st);
-            default: break;
-        }
-    } else if (nt == 64) {
-        switch (W) {
-            case 1: return launch_w<1, 64>(L, smem, st);
-            case 2: return launch_w<2, 64>(L, smem, st);
-            default: break;
-        }
-    } else if (nt == 256) {
-        switch (W) {
-            case 1: return launch_w<1, 256>(L, smem, st);
-            case 3: return launch_w<3, 256>(L, smem, st);
-            default: break;
-        }
-    }
-    return cudaErrorInvalidValue;
+    return launch_search_w(L, W, nt, dense, smem, st);
 }
 
 cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st) {
