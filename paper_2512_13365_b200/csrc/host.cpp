@@ -184,55 +184,29 @@ struct tcse_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t owned_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    int nt = 64;
+    int nt = 0;
     int rank = 0, world = 1;
     tcse_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
     DBuf err;  // int32 err + err_pos
     DBuf slots, rng;  // prep_kernel -> search_kernel hand-off
+    // launch groups beyond the first run on their own streams, forked from and
+    // joined back into `stream` with events
+    cudaStream_t aux[kMaxSys] = {};
+    cudaEvent_t fork = nullptr, join[kMaxSys] = {};
 };
 
 // one system prepared on the device
 struct DevSys {
     HostSys h;
-    int W = 1;
+    int W = 1;         // mask words the kernel is instantiated with
+    int nt = 64;       // block size (threads per process)
+    bool dense = true; // Greedy-Intersections form
     DBuf masks, keys, cnts;
     int base_m = 0;
 };
 
 namespace {
-
-// extra_vars: fresh variables a caller-supplied prefix may add beyond the
-// search bound.  Every search substitution replaces c >= 2 occurrences and
-// the total term count can drop by at most naive (rows never empty), so a
-// search creates at most naive/2 fresh variables; an arbitrary replayed
-// prefix may use c = 1 pairs, hence the extra allowance.
-int prepare(tcse_ctx* ctx, const tcse_system* s, int W, DevSys* d, int extra_vars = 0) {
-    int rc = validate_system(s, &d->h);
-    if (rc)
-        return rc;
-    d->h.vcap = d->h.n_x + d->h.naive / 2 + extra_vars + 1;
-    d->W = W;
-    const auto masks = pack_masks(d->h, W);
-    CU(d->masks.reserve(std::max<size_t>(8, masks.size() * 8)));
-    if (!masks.empty())
-        CU(cudaMemcpyAsync(d->masks.p, masks.data(), masks.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CU(d->keys.reserve(size_t(d->h.mcap) * 4));
-    CU(d->cnts.reserve(size_t(d->h.mcap) * 2));
-    return TCSE_OK;
-}
-
-// block size the kernel is instantiated for at this word count
-int pick_nt(tcse_ctx* ctx, int W) {
-    int nt = ctx->nt;
-    if (nt == 32 && W != 1)
-        nt = 64;
-    if (nt == 64 && W > 2)
-        nt = 128;
-    if (nt == 256 && W != 1 && W != 3)
-        nt = 128;
-    return nt;
-}
 
 int coin_words_for(const HostSys& h) {
     // gi coin bits: all coins of a step fit for typical states (sum of
@@ -249,31 +223,73 @@ int gi_dense_for(const HostSys& h) {
     return h.mcap <= 640 ? 1 : 0;
 }
 
-// one gi form per launch: dense only if every system of the launch prefers it
-bool launch_dense(const std::vector<DevSys*>& sys) {
-    bool dense = true;
-    for (auto* d : sys)
-        dense = dense && gi_dense_for(d->h);
-    return dense;
+// (W, NT) pairs search_kernel is instantiated for (search.cu launch_search_w)
+bool instantiated(int W, int nt) {
+    switch (nt) {
+        case 32: return W == 1;
+        case 64: return W <= 2;
+        case 128: return W == 1 || W == 2 || W == 3 || W == 4 || W == 8;
+        case 256: return W == 1 || W == 3;
+        default: return false;
+    }
 }
 
-int smem_for(int nt, int W, const std::vector<DevSys*>& sys) {
-    const bool dense = launch_dense(sys);
-    u32 mx = 0;
-    for (auto* d : sys) {
-        Lay L;
-        mx = std::max(mx, carve(&L, W, nt, d->h.vcap, d->h.mcap, d->h.n_e, coin_words_for(d->h), dense));
-    }
-    return int(mx);
+// Launch shape of one system: mask words, block size (one warp for small
+// candidate lists, wider blocks for long ones) and the gi form.  None of
+// these changes results.
+void choose_launch(const tcse_ctx* ctx, DevSys* d) {
+    d->W = launch_words(d->h.w_need);
+    d->dense = gi_dense_for(d->h) != 0;
+    int nt = ctx->nt;
+    if (nt == 0)
+        nt = (d->W == 1 && d->h.mcap <= 96) ? 32 : ((d->W <= 2 && d->h.mcap <= 1024) ? 64 : 128);
+    if (!instantiated(d->W, nt))
+        nt = 128;
+    d->nt = nt;
+}
+
+int smem_one(const DevSys& d) {
+    Lay L;
+    return int(carve(&L, d.W, d.nt, d.h.vcap, d.h.mcap, d.h.n_e, coin_words_for(d.h), d.dense));
+}
+
+// extra_vars: fresh variables a caller-supplied prefix may add beyond the
+// search bound.  Every search substitution replaces c >= 2 occurrences and
+// the total term count can drop by at most naive (rows never empty), so a
+// search creates at most naive/2 fresh variables; an arbitrary replayed
+// prefix may use c = 1 pairs, hence the extra allowance.
+int prepare(tcse_ctx* ctx, const tcse_system* s, DevSys* d, int extra_vars = 0) {
+    int rc = validate_system(s, &d->h);
+    if (rc)
+        return rc;
+    d->h.vcap = d->h.n_x + d->h.naive / 2 + extra_vars + 1;
+    choose_launch(ctx, d);
+    const int W = d->W;
+    const auto masks = pack_masks(d->h, W);
+    CU(d->masks.reserve(std::max<size_t>(8, masks.size() * 8)));
+    if (!masks.empty())
+        CU(cudaMemcpyAsync(d->masks.p, masks.data(), masks.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(d->keys.reserve(size_t(d->h.mcap) * 4));
+    CU(d->cnts.reserve(size_t(d->h.mcap) * 2));
+    return TCSE_OK;
 }
 
 // slot records + seeded mt19937_64 states for `blocks` processes
-int attach_prep(tcse_ctx* ctx, LaunchDesc* L) {
-    const size_t b = size_t(std::max(L->total_blocks, 1));
+int reserve_prep(tcse_ctx* ctx, int blocks) {
+    const size_t b = size_t(std::max(blocks, 1));
     CU(ctx->slots.reserve(b * sizeof(SlotRec)));
     CU(ctx->rng.reserve(b * 312 * 8));
-    L->slots = ctx->slots.as<SlotRec>();
-    L->rng = ctx->rng.as<u64>();
+    return TCSE_OK;
+}
+
+int attach_prep(tcse_ctx* ctx, LaunchDesc* L, int block_offset = 0) {
+    if (block_offset == 0) {
+        const int rc = reserve_prep(ctx, L->total_blocks);
+        if (rc)
+            return rc;
+    }
+    L->slots = ctx->slots.as<SlotRec>() + block_offset;
+    L->rng = ctx->rng.as<u64>() + size_t(block_offset) * 312;
     return TCSE_OK;
 }
 
@@ -298,7 +314,7 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.naive = d.h.naive;
     sd.words = d.h.w_need;
     sd.coin_words = coin_words_for(d.h);
-    sd.gi_dense = gi_dense_for(d.h);  // overwritten with the launch's form
+    sd.gi_dense = d.dense ? 1 : 0;
     sd.vcap = d.h.vcap;
     sd.mcap = d.h.mcap;
     sd.sub_cap = d.h.naive / 2 + 1;
@@ -337,8 +353,8 @@ int run_dump(tcse_ctx* ctx, DevSys& d, const u32* d_prefix, int n_prefix, int mi
     int prc = attach_prep(ctx, &L);
     if (prc)
         return prc;
-    L.sys[0].gi_dense = launch_dense(v);
-    CU(launch_search(L, d.W, pick_nt(ctx, d.W), launch_dense(v), smem_for(pick_nt(ctx, d.W), d.W, v), ctx->stream));
+    L.sys[0].gi_dense = d.dense;
+    CU(launch_search(L, d.W, d.nt, d.dense, smem_one(d), ctx->stream));
     int rc = check_err(ctx);
     if (rc)
         return rc;
@@ -472,9 +488,9 @@ tcse_ctx* tcse_create(int32_t device) {
     }
     auto* ctx = new tcse_ctx;
     ctx->device = device;
-    ctx->nt = env_int("TCSE_NT", 64);
-    if (ctx->nt != 32 && ctx->nt != 64 && ctx->nt != 128 && ctx->nt != 256)
-        ctx->nt = 64;
+    ctx->nt = env_int("TCSE_NT", 0);  // 0 = by problem size
+    if (ctx->nt != 0 && ctx->nt != 32 && ctx->nt != 64 && ctx->nt != 128 && ctx->nt != 256)
+        ctx->nt = 0;
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
         ctx->err.reserve(8) != cudaSuccess) {
@@ -497,6 +513,14 @@ void tcse_destroy(tcse_ctx* ctx) {
         cudaEventDestroy(ctx->ev0);
     if (ctx->ev1)
         cudaEventDestroy(ctx->ev1);
+    for (int g = 0; g < kMaxSys; ++g) {
+        if (ctx->aux[g])
+            cudaStreamDestroy(ctx->aux[g]);
+        if (ctx->join[g])
+            cudaEventDestroy(ctx->join[g]);
+    }
+    if (ctx->fork)
+        cudaEventDestroy(ctx->fork);
     delete ctx;
 }
 
@@ -529,7 +553,7 @@ int tcse_count_pairs(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* pre
     int rc = validate_system(sys, &probe);
     if (rc)
         return rc;
-    rc = prepare(ctx, sys, launch_words(probe.w_need), &d, n_prefix);
+    rc = prepare(ctx, sys, &d, n_prefix);
     if (rc)
         return rc;
     rc = base_candidates(ctx, d);
@@ -590,8 +614,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     int rc = validate_system(sys, &probe);
     if (rc)
         return rc;
-    const int W = launch_words(probe.w_need);
-    rc = prepare(ctx, sys, W, &d, n_prefix);
+    rc = prepare(ctx, sys, &d, n_prefix);
     if (rc)
         return rc;
     rc = base_candidates(ctx, d);
@@ -641,8 +664,8 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     if (rc)
         return rc;
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
-    L.sys[0].gi_dense = launch_dense(v);
-    CU(launch_search(L, W, pick_nt(ctx, W), launch_dense(v), smem_for(pick_nt(ctx, W), W, v), ctx->stream));
+    L.sys[0].gi_dense = d.dense;
+    CU(launch_search(L, d.W, d.nt, d.dense, smem_one(d), ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
     rc = check_err(ctx);
     if (rc)
@@ -707,8 +730,14 @@ struct tcse_search {
     std::vector<uint64_t> salts;
     tcse_iter_cb cb = nullptr;
     void* user = nullptr;
-    int n = 0, p0 = 0, n_local = 0, Wmax = 1, nt = 128, smem = 0, hist_n = 1;
-    bool dense = true;
+    int n = 0, p0 = 0, n_local = 0, hist_n = 1;
+    struct Group {
+        int W, nt;
+        bool dense;
+        int smem;
+        std::vector<int> sys;
+    };
+    std::vector<Group> groups;
     double weight_total = 0.0;
     std::unique_ptr<DevSys[]> dev;
     std::unique_ptr<Pool[]> pool;
@@ -767,29 +796,36 @@ int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_sys
     S->dev.reset(new DevSys[size_t(n_systems)]);
     S->pool.reset(new Pool[size_t(n_systems)]);
     for (int s = 0; s < n_systems; ++s) {
-        HostSys probe;
-        rc = validate_system(&systems[s], &probe);
-        if (rc)
-            return rc;
-        S->Wmax = std::max(S->Wmax, launch_words(probe.w_need));
-    }
-    S->nt = pick_nt(ctx, S->Wmax);
-    std::vector<DevSys*> dptr;
-    for (int s = 0; s < n_systems; ++s) {
         DevSys& d = S->dev[size_t(s)];
-        rc = prepare(ctx, &systems[s], S->Wmax, &d);
+        rc = prepare(ctx, &systems[s], &d);
         if (rc)
             return rc;
-        S->h2d += uint64_t(d.h.n_x) * 2 * uint64_t(S->Wmax) * 8;
+        S->h2d += uint64_t(d.h.n_x) * 2 * uint64_t(d.W) * 8;
         rc = base_candidates(ctx, d);
         if (rc)
             return rc;
-        dptr.push_back(&d);
+        // launch groups: systems with the same kernel instantiation share a launch
+        bool placed = false;
+        for (auto& g : S->groups)
+            if (g.W == d.W && g.nt == d.nt && g.dense == d.dense) {
+                g.sys.push_back(s);
+                g.smem = std::max(g.smem, smem_one(d));
+                placed = true;
+            }
+        if (!placed)
+            S->groups.push_back({d.W, d.nt, d.dense, smem_one(d), {s}});
     }
-    S->smem = smem_for(S->nt, S->Wmax, dptr);
-    S->dense = launch_dense(dptr);
-    if (S->smem > 227 * 1024 - 1024)
-        return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", S->smem);
+    for (const auto& g : S->groups)
+        if (g.smem > 227 * 1024 - 1024)
+            return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", g.smem);
+    for (size_t g = 1; g < S->groups.size(); ++g) {
+        if (!ctx->aux[g - 1])
+            CU(cudaStreamCreateWithFlags(&ctx->aux[g - 1], cudaStreamNonBlocking));
+        if (!ctx->join[g - 1])
+            CU(cudaEventCreateWithFlags(&ctx->join[g - 1], cudaEventDisableTiming));
+    }
+    if (!ctx->fork)
+        CU(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
     for (int s = 0; s < n_systems; ++s) {
         Pool& P = S->pool[size_t(s)];
         const DevSys& d = S->dev[size_t(s)];
@@ -874,55 +910,78 @@ int search_step_begin(tcse_search* S, void* send_ext) {
         return TCSE_OK;
     CU(cudaSetDevice(ctx->device));
     const int iteration = ++S->iteration;
-    LaunchDesc L;
-    std::memset(&L, 0, sizeof L);
-    int blocks = 0;
-    for (int s : S->act) {
-        const DevSys& d = S->dev[size_t(s)];
-        Pool& P = S->pool[size_t(s)];
-        SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
-        sd.mode = kModeSearch;
-        sd.base_keys = d.keys.as<u32>();
-        sd.base_cnts = d.cnts.as<u16>();
-        sd.base_m = d.base_m;
-        sd.n_local = S->n_local;
-        sd.p0 = S->p0;
-        sd.block_begin = blocks;
-        sd.master_seed = S->cfg.master_seed;
-        sd.salt = S->salts[size_t(s)];
-        sd.iteration = iteration;
-        sd.forced = S->cfg.forced_strategy;
-        for (int k = 0; k < 7; ++k)
-            sd.weights[k] = S->cfg.strategy_weights[k];
-        sd.weight_total = S->weight_total;
-        for (int k = 0; k < 4; ++k)
-            sd.mix[k] = S->cfg.mix_weights[k];
-        sd.reinit = iteration >= 2 ? P.reinit.as<u8>() + S->p0 : nullptr;
-        sd.inc_keys = P.inc_keys.as<u32>();
-        sd.inc_len = S->hinc[size_t(s)].len;
-        sd.out_cost = P.cost.as<int32_t>();
-        sd.out_len = P.len.as<int32_t>();
-        sd.out_own = P.own.as<int32_t>();
-        sd.out_strategy = P.strat.as<int32_t>();
-        sd.out_seed = P.seed.as<u64>();
-        sd.out_wops = P.wops.as<u64>();
-        sd.out_subs = P.subs.as<u32>();
-        L.sys[L.nsys++] = sd;
-        blocks += S->n_local;
-    }
-    L.total_blocks = blocks;
-    if ((rc = attach_prep(ctx, &L)))
+    // ---- K0 + K1 per launch group; groups after the first on their own
+    // streams (forked from / joined into the context stream)
+    int total = 0;
+    for (int s : S->act)
+        total += S->n_local;
+    if ((rc = reserve_prep(ctx, total)))
         return rc;
     CU(cudaEventRecord(S->es0, ctx->stream));
-    if (blocks > 0) {
-        CU(cudaEventRecord(ctx->ev0, ctx->stream));
-        for (int t = 0; t < L.nsys; ++t)
-            L.sys[t].gi_dense = S->dense;
-        CU(launch_search(L, S->Wmax, S->nt, S->dense, S->smem, ctx->stream));
-        CU(cudaEventRecord(ctx->ev1, ctx->stream));
+    CU(cudaEventRecord(ctx->ev0, ctx->stream));
+    CU(cudaEventRecord(ctx->fork, ctx->stream));
+    int block_off = 0, n_aux = 0;
+    for (size_t gi = 0; gi < S->groups.size(); ++gi) {
+        const auto& g = S->groups[gi];
+        LaunchDesc L;
+        std::memset(&L, 0, sizeof L);
+        int blocks = 0;
+        for (int s : g.sys) {
+            if (!S->active[size_t(s)])
+                continue;
+            const DevSys& d = S->dev[size_t(s)];
+            Pool& P = S->pool[size_t(s)];
+            SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
+            sd.mode = kModeSearch;
+            sd.base_keys = d.keys.as<u32>();
+            sd.base_cnts = d.cnts.as<u16>();
+            sd.base_m = d.base_m;
+            sd.n_local = S->n_local;
+            sd.p0 = S->p0;
+            sd.block_begin = blocks;
+            sd.master_seed = S->cfg.master_seed;
+            sd.salt = S->salts[size_t(s)];
+            sd.iteration = iteration;
+            sd.forced = S->cfg.forced_strategy;
+            for (int k = 0; k < 7; ++k)
+                sd.weights[k] = S->cfg.strategy_weights[k];
+            sd.weight_total = S->weight_total;
+            for (int k = 0; k < 4; ++k)
+                sd.mix[k] = S->cfg.mix_weights[k];
+            sd.reinit = iteration >= 2 ? P.reinit.as<u8>() + S->p0 : nullptr;
+            sd.inc_keys = P.inc_keys.as<u32>();
+            sd.inc_len = S->hinc[size_t(s)].len;
+            sd.out_cost = P.cost.as<int32_t>();
+            sd.out_len = P.len.as<int32_t>();
+            sd.out_own = P.own.as<int32_t>();
+            sd.out_strategy = P.strat.as<int32_t>();
+            sd.out_seed = P.seed.as<u64>();
+            sd.out_wops = P.wops.as<u64>();
+            sd.out_subs = P.subs.as<u32>();
+            sd.gi_dense = g.dense ? 1 : 0;
+            L.sys[L.nsys++] = sd;
+            blocks += S->n_local;
+        }
+        if (blocks == 0)
+            continue;
+        L.total_blocks = blocks;
+        if ((rc = attach_prep(ctx, &L, block_off)))
+            return rc;
+        block_off += blocks;
+        cudaStream_t st = ctx->stream;
+        if (n_aux + 1 <= int(S->groups.size()) - 1 && block_off > blocks) {
+            st = ctx->aux[n_aux];
+            CU(cudaStreamWaitEvent(st, ctx->fork, 0));
+        }
+        CU(launch_search(L, g.W, g.nt, g.dense, g.smem, st));
+        if (st != ctx->stream)
+            CU(cudaEventRecord(ctx->join[n_aux++], st));
         ++S->launches;
         S->processes += uint64_t(blocks);
     }
+    for (int a = 0; a < n_aux; ++a)
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->join[a], 0));
+    CU(cudaEventRecord(ctx->ev1, ctx->stream));
     S->tx = std::chrono::steady_clock::now();
     int32_t* send = send_ext ? static_cast<int32_t*>(send_ext) : S->send.as<int32_t>();
     XchgLaunch XL;

@@ -806,7 +806,7 @@ struct St {
         last_coins = D;
         double best_s = -1.0;
         int best_q = 0x7fffffff;
-        if (!dense && D <= lay.coin_cap) {
+        if (!dense) {
             u32* aoff = sp<u32>(lay.aoff);
             u32* cursor = sp<u32>(lay.cursor);
             u32* bs = sp<u32>(lay.bs);
@@ -829,36 +829,53 @@ struct St {
                     alist[b0 + y + 1] = t;
                 }
             }
-            draw_coins(D);  // barrier-separated clear, ends with a barrier
-            for (int q = tid; q < m; q += NT) {
-                const u32 kq = ks[q];
-                const int qi = key_i(kq), qj = key_j(kq);
-                const int ai = int(aoff[qi]), nai = int(nA[qi]), bi = int(bs[qi]), li = nai + int(nB[qi]);
-                const int aj = int(aoff[qj]), naj = int(nA[qj]), bj = int(bs[qj]), lj = naj + int(nB[qj]);
-                u32 ptr = qbase[q];
-                double f = 0.0;
-                int prev = 0, pi = 0, pj = 0;
-                for (;;) {
-                    const int xi = pi < li ? (pi < nai ? int(alist[ai + pi]) : bi + (pi - nai)) : 0x7fffffff;
-                    const int xj = pj < lj ? (pj < naj ? int(alist[aj + pj]) : bj + (pj - naj)) : 0x7fffffff;
-                    const int s = min(xi, xj);
-                    pi += xi == s;
-                    pj += xj == s;
-                    f = add_run(f, prev, s == 0x7fffffff ? m : s, wp);
-                    if (s == 0x7fffffff)
-                        break;
-                    prev = s + 1;
-                    if (s != q) {
-                        if ((coin[ptr >> 5] >> (ptr & 31u)) & 1u)
-                            f = __dadd_rn(f, wbt[c[s]]);
-                        ++ptr;
+            // coins in chunks of candidates whose coins fit the buffer
+            const u32 cap = lay.coin_cap;
+            int q_lo = 0;
+            while (q_lo < m) {
+                const u32 c0 = qbase[q_lo];
+                int lo = q_lo + 1, hi = m;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (qbase[mid] - c0 <= cap)
+                        lo = mid;
+                    else
+                        hi = mid - 1;
+                }
+                const int q_hi = lo;
+                draw_coins(qbase[q_hi] - c0);  // barrier-separated clear, ends with a barrier
+                for (int q = q_lo + tid; q < q_hi; q += NT) {
+                    const u32 kq = ks[q];
+                    const int qi = key_i(kq), qj = key_j(kq);
+                    const int ai = int(aoff[qi]), nai = int(nA[qi]), bi = int(bs[qi]), li = nai + int(nB[qi]);
+                    const int aj = int(aoff[qj]), naj = int(nA[qj]), bj = int(bs[qj]), lj = naj + int(nB[qj]);
+                    u32 ptr = qbase[q] - c0;
+                    double f = 0.0;
+                    int prev = 0, pi = 0, pj = 0;
+                    for (;;) {
+                        const int xi = pi < li ? (pi < nai ? int(alist[ai + pi]) : bi + (pi - nai)) : 0x7fffffff;
+                        const int xj = pj < lj ? (pj < naj ? int(alist[aj + pj]) : bj + (pj - naj)) : 0x7fffffff;
+                        const int s = min(xi, xj);
+                        pi += xi == s;
+                        pj += xj == s;
+                        f = add_run(f, prev, s == 0x7fffffff ? m : s, wp);
+                        if (s == 0x7fffffff)
+                            break;
+                        prev = s + 1;
+                        if (s != q) {
+                            if ((coin[ptr >> 5] >> (ptr & 31u)) & 1u)
+                                f = __dadd_rn(f, wbt[c[s]]);
+                            ++ptr;
+                        }
+                    }
+                    const double h = __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, f));
+                    if (h > best_s || best_q == 0x7fffffff) {
+                        best_s = h;
+                        best_q = q;
                     }
                 }
-                const double h = __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, f));
-                if (h > best_s || best_q == 0x7fffffff) {
-                    best_s = h;
-                    best_q = q;
-                }
+                __syncthreads();
+                q_lo = q_hi;
             }
         } else {
             // the reference loop itself, coins in chunks; each thread carries
