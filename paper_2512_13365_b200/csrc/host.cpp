@@ -229,7 +229,7 @@ bool instantiated(int W, int nt) {
         case 32: return W == 1;
         case 64: return W <= 2;
         case 128: return W == 1 || W == 2 || W == 3 || W == 4 || W == 8;
-        case 256: return W == 1 || W == 3;
+        case 256: return W >= 1 && W <= 4;
         default: return false;
     }
 }
@@ -241,8 +241,16 @@ void choose_launch(const tcse_ctx* ctx, DevSys* d) {
     d->W = launch_words(d->h.w_need);
     d->dense = gi_dense_for(d->h) != 0;
     int nt = ctx->nt;
-    if (nt == 0)
-        nt = (d->W == 1 && d->h.mcap <= 96) ? 32 : ((d->W <= 2 && d->h.mcap <= 1024) ? 64 : 128);
+    if (nt == 0) {
+        if (d->W == 1 && d->h.mcap <= 96)
+            nt = 32;  // one warp per process
+        else if (d->W <= 2 && d->h.mcap <= 1024)
+            nt = 64;
+        else if (d->h.mcap <= 1024)
+            nt = 128;
+        else
+            nt = 256;  // long candidate lists: more candidates scored in parallel
+    }
     if (!instantiated(d->W, nt))
         nt = 128;
     d->nt = nt;

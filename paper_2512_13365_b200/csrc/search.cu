@@ -1529,7 +1529,9 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int 
     TCSE_CASE(4, 128)
     TCSE_CASE(8, 128)
     TCSE_CASE(1, 256)
+    TCSE_CASE(2, 256)
     TCSE_CASE(3, 256)
+    TCSE_CASE(4, 256)
 #undef TCSE_CASE
     return cudaErrorInvalidValue;
 }
