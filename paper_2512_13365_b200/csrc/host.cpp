@@ -189,7 +189,7 @@ struct tcse_ctx {
     tcse_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
     DBuf err;  // int32 err + err_pos
-    DBuf slots, rng;  // prep_kernel -> search_kernel hand-off
+    DBuf slots, rng, perm, hist;  // prep_kernel -> search_kernel hand-off
     // launch groups beyond the first run on their own streams, forked from and
     // joined back into `stream` with events
     cudaStream_t aux[kMaxSys] = {};
@@ -287,10 +287,12 @@ int reserve_prep(tcse_ctx* ctx, int blocks) {
     const size_t b = size_t(std::max(blocks, 1));
     CU(ctx->slots.reserve(b * sizeof(SlotRec)));
     CU(ctx->rng.reserve(b * 312 * 8));
+    CU(ctx->perm.reserve(b * 4));
+    CU(ctx->hist.reserve(sizeof(int32_t) * 16 * kMaxSys * (kMaxSys + 1)));
     return TCSE_OK;
 }
 
-int attach_prep(tcse_ctx* ctx, LaunchDesc* L, int block_offset = 0) {
+int attach_prep(tcse_ctx* ctx, LaunchDesc* L, int block_offset = 0, int group = 0) {
     if (block_offset == 0) {
         const int rc = reserve_prep(ctx, L->total_blocks);
         if (rc)
@@ -298,6 +300,12 @@ int attach_prep(tcse_ctx* ctx, LaunchDesc* L, int block_offset = 0) {
     }
     L->slots = ctx->slots.as<SlotRec>() + block_offset;
     L->rng = ctx->rng.as<u64>() + size_t(block_offset) * 312;
+    // strategy-grouped launch order (search mode; TCSE_ORDER=0 disables)
+    static const int order = env_int("TCSE_ORDER", 1);
+    if (order && L->sys[0].mode == kModeSearch) {
+        L->perm = ctx->perm.as<int32_t>() + block_offset;
+        L->hist = ctx->hist.as<int32_t>() + 16 * kMaxSys * group;  // one per concurrent launch group
+    }
     return TCSE_OK;
 }
 
@@ -973,7 +981,7 @@ int search_step_begin(tcse_search* S, void* send_ext) {
         if (blocks == 0)
             continue;
         L.total_blocks = blocks;
-        if ((rc = attach_prep(ctx, &L, block_off)))
+        if ((rc = attach_prep(ctx, &L, block_off, int(gi))))
             return rc;
         block_off += blocks;
         cudaStream_t st = ctx->stream;

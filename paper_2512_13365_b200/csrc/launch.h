@@ -104,6 +104,8 @@ struct LaunchDesc {
     int32_t total_blocks;
     SlotRec* slots;  // [total_blocks]
     u64* rng;        // [total_blocks][312] seeded mt19937_64 states
+    int32_t* perm;   // [total_blocks] launch order -> block (grouped by strategy), or null
+    int32_t* hist;   // [kMaxSys][16] strategy histogram + placement cursors
     SysDesc sys[kMaxSys];
 };
 

@@ -1061,13 +1061,16 @@ struct MinBlocks {
 
 template <int W, int NT, bool GID>
 __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const __grid_constant__ LaunchDesc L) {
+    // launch order -> process block: blocks of one strategy run together, most
+    // expensive strategies first (instruction-cache locality, shorter tail)
+    const int blk = L.perm ? L.perm[blockIdx.x] : int(blockIdx.x);
     int s = 0;
 #pragma unroll
     for (int t = 1; t < kMaxSys; ++t)
-        if (t < L.nsys && int(blockIdx.x) >= L.sys[t].block_begin)
+        if (t < L.nsys && blk >= L.sys[t].block_begin)
             s = t;
     const SysDesc& sd = L.sys[s];
-    const int lp = int(blockIdx.x) - sd.block_begin;
+    const int lp = blk - sd.block_begin;
     if (lp >= sd.n_local)
         return;
     const int tid = threadIdx.x;
@@ -1076,7 +1079,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     __shared__ SlotRec s_slot;
     if (tid == 0) {
         carve(&lay, W, NT, sd.vcap, sd.mcap, sd.n_e, sd.coin_words, sd.gi_dense);
-        s_slot = L.slots[blockIdx.x];
+        s_slot = L.slots[blk];
     }
     __syncthreads();
     {
@@ -1094,7 +1097,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         }
         if (s_slot.rng) {
             u64* mt = sp<u64>(lay.mt);
-            const u64* src = L.rng + size_t(blockIdx.x) * 312;
+            const u64* src = L.rng + size_t(blk) * 312;
             for (int t = tid; t < 312; t += NT)
                 mt[t] = src[t];
         }
@@ -1300,8 +1303,33 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     r.p_greedy = sl.p_greedy;
     r.seed = sl.seed;
     L.slots[b] = r;
+    if (L.hist)
+        atomicAdd(&L.hist[s * 16 + st], 1);
     if (rng)
         mt_seed(L.rng + size_t(b) * 312, sl.seed);
+}
+
+// launch position of every block: per system, strategies in the order
+// gp, gi, mix, gr, ga, wr, g (roughly decreasing cost), any order within one
+__global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ LaunchDesc L) {
+    const int b = int(blockIdx.x * blockDim.x + threadIdx.x);
+    if (b >= L.total_blocks)
+        return;
+    int s = 0;
+#pragma unroll
+    for (int t = 1; t < kMaxSys; ++t)
+        if (t < L.nsys && b >= L.sys[t].block_begin)
+            s = t;
+    const SysDesc& sd = L.sys[s];
+    if (b - sd.block_begin >= sd.n_local)
+        return;
+    const int order[7] = {TCSE_GREEDY_POTENTIAL, TCSE_GREEDY_INTERSECTIONS, TCSE_MIXED, TCSE_GREEDY_RANDOM,
+                          TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY};
+    const int st = L.slots[b].strategy;
+    int base = sd.block_begin;
+    for (int k = 0; k < 7 && order[k] != st; ++k)
+        base += L.hist[s * 16 + order[k]];
+    L.perm[base + atomicAdd(&L.hist[s * 16 + 8 + st], 1)] = b;
 }
 
 // ----------------------------------------------------------------- K2
@@ -1537,7 +1565,15 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int 
 }
 
 cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
-    prep_kernel<<<(L.total_blocks + 127) / 128, 128, 0, st>>>(L);
+    const int g = (L.total_blocks + 127) / 128;
+    if (L.hist) {
+        cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * 16 * kMaxSys, st);
+        if (e != cudaSuccess)
+            return e;
+    }
+    prep_kernel<<<g, 128, 0, st>>>(L);
+    if (L.perm)
+        place_kernel<<<g, 128, 0, st>>>(L);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
