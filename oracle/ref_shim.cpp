@@ -323,6 +323,43 @@ int ref_optimize_scheme_json(const char* scheme_json, const tcse_search_config* 
     });
 }
 
+// emit_slp (io.hpp:352-393) of a report (parse_report, io.hpp:268-291) for a scheme
+int ref_emit_slp(const char* scheme_json, const char* report_json, char* out, int32_t cap, int32_t* n_out) {
+    return guarded([&]() -> int {
+        const auto text = emit_slp(parse_report(report_json), parse_scheme(scheme_json));
+        *n_out = int32_t(text.size());
+        if (int(text.size()) + 1 > cap)
+            return fail(TCSE_ECAPACITY, "buffer too small");
+        std::memcpy(out, text.c_str(), text.size() + 1);
+        return TCSE_OK;
+    });
+}
+
+// combine_componentwise (parallel_search.hpp:522-547) of several report JSONs
+// separated by '\x1e', back to report JSON
+int ref_combine_json(const char* reports, char* out, int32_t cap, int32_t* n_out) {
+    return guarded([&]() -> int {
+        std::vector<SearchReport> rs;
+        std::string all(reports), cur;
+        for (char ch : all) {
+            if (ch == '\x1e') {
+                rs.push_back(parse_report(cur));
+                cur.clear();
+            } else {
+                cur += ch;
+            }
+        }
+        if (!cur.empty())
+            rs.push_back(parse_report(cur));
+        const auto text = report_to_json(combine_componentwise(rs));
+        *n_out = int32_t(text.size());
+        if (int(text.size()) + 1 > cap)
+            return fail(TCSE_ECAPACITY, "buffer too small");
+        std::memcpy(out, text.c_str(), text.size() + 1);
+        return TCSE_OK;
+    });
+}
+
 // naive_scheme / random_flip (scheme.hpp:161-276) for fixture generation
 int ref_flipped_naive_json(int32_t m, int32_t n, int32_t p, int32_t flips, uint64_t seed,
                            char* out, int32_t cap, int32_t* n_out) {

@@ -24,6 +24,7 @@ from ._abi import (STRATEGY_NAMES, STRATEGY_SHORT, DEFAULT_MIX, DEFAULT_WEIGHTS,
                    make_process_config, make_record, make_search_config, make_system, record_subs)
 from .scheme import (SchemeError, extract_systems, load_scheme, naive_cost, parse_scheme,
                      scheme_digest, verify_brent)
+from .slp import combine_componentwise, count_slp_operators, emit_slp, emit_slp_system, parse_report
 
 __all__ = [
     "TcseError", "LinearSystem", "ProcessConfig", "SearchConfig", "SolutionRecord", "Device",
@@ -31,6 +32,7 @@ __all__ = [
     "verify_record", "report_to_json", "strategy_from_string", "library_path",
     "parse_scheme", "load_scheme", "extract_systems", "naive_cost", "scheme_digest", "verify_brent",
     "SchemeError", "STRATEGY_NAMES", "STRATEGY_SHORT", "DEFAULT_WEIGHTS",
+    "emit_slp", "emit_slp_system", "parse_report", "combine_componentwise", "count_slp_operators",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -522,4 +524,6 @@ def report_to_json(report):
         }
     j = {"scheme_digest": report["scheme_digest"], "config": jc, "components": comps,
          "total": report["total"], "iterations": report["iterations"]}
+    if report.get("combined"):
+        j["combined"] = True
     return _dump(j) + "\n"

@@ -59,6 +59,31 @@ def main():
         rc = ref.ref_optimize_scheme_json(text.encode(), C.byref(c), 4, buf, len(buf), C.byref(n))
         assert rc == 0, ref.ref_last_error()
         g["reports"][name] = dict(cfg=dict(cfg), json=buf.value.decode())
+    # emit_slp (io.hpp:352-393) of each report, and combine_componentwise of two
+    # laderman reports (parallel_search.hpp:522-547), from the reference
+    ref.ref_emit_slp.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, C.POINTER(C.c_int32)]
+    ref.ref_combine_json.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.POINTER(C.c_int32)]
+    for name, r in g["reports"].items():
+        with open(os.path.join(HERE, "schemes", name + ".json")) as f:
+            text = f.read()
+        buf = C.create_string_buffer(1 << 22)
+        n = C.c_int32()
+        assert ref.ref_emit_slp(text.encode(), r["json"].encode(), buf, len(buf), C.byref(n)) == 0
+        r["slp"] = buf.value.decode()
+    with open(os.path.join(HERE, "schemes", "laderman.json")) as f:
+        text = f.read()
+    other = {}
+    for seed in (3, 4):
+        cfg = T.SearchConfig(n_processes=16, patience=2, master_seed=seed)
+        buf = C.create_string_buffer(1 << 22)
+        n = C.c_int32()
+        assert ref.ref_optimize_scheme_json(text.encode(), C.byref(cfg.to_c()), 4, buf, len(buf), C.byref(n)) == 0
+        other[seed] = buf.value.decode()
+    buf = C.create_string_buffer(1 << 22)
+    n = C.c_int32()
+    joined = (other[3] + "\x1e" + other[4]).encode()
+    assert ref.ref_combine_json(joined, buf, len(buf), C.byref(n)) == 0, ref.ref_last_error()
+    g["combine"] = dict(inputs=[other[3], other[4]], json=buf.value.decode())
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(g, f, separators=(",", ":"))
         f.write("\n")
