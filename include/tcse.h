@@ -124,6 +124,41 @@ typedef struct tcse_record {
     uint64_t seed;
 } tcse_record;
 
+/* A matrix multiplication scheme (m, n, p : r) with ternary coefficients
+ * (Scheme, scheme.hpp:20-27), row-major int8 in {-1, 0, 1}:
+ * u is r x (m*n), v is r x (n*p), w is (m*p) x r. */
+typedef struct tcse_scheme {
+    int32_t m, n, p, r;
+    const int8_t* u;
+    const int8_t* v;
+    const int8_t* w;
+} tcse_scheme;
+
+/* FlipModeConfig (parallel_search.hpp:24-29) */
+typedef struct tcse_flip_config {
+    int32_t m_schemes;
+    int32_t flips_min;
+    int32_t flips_max;
+    int32_t reserved;
+} tcse_flip_config;
+
+/* optimize_with_flips result (SearchReport of flip mode): the carried scheme
+ * (caller-allocated u/v/w with the input's shapes), the three component
+ * records (caller-allocated, cap >= r * max(m*n, n*p) suffices), their naive
+ * costs on the carried scheme, and the winning scheme's id: slot 0 =
+ * "original", else "flip-<scheme_iteration>-<scheme_slot>". */
+typedef struct tcse_flip_result {
+    int8_t* u;
+    int8_t* v;
+    int8_t* w;
+    tcse_record comp[3];
+    int32_t naive[3];
+    int32_t iterations;
+    int32_t scheme_iteration;
+    int32_t scheme_slot;
+    int32_t total;
+} tcse_flip_result;
+
 /* execution counters (not part of any reference result) */
 typedef struct tcse_stats {
     uint64_t steps;        /* selected substitutions (replayed prefixes excluded) */
@@ -247,6 +282,16 @@ int tcse_search_step_end(tcse_search* search, const void* recv_dev, int32_t* n_a
 int tcse_search_result(tcse_search* search, tcse_record* best, int32_t* iterations,
                        tcse_stats* stats);
 void tcse_search_destroy(tcse_search* search);
+
+/* optimize_with_flips (parallel_search.hpp:354-518) with the search on the
+ * device: every iteration M scheme variants (slot 0 the input, the others
+ * random_flip chains seeded by mix_seed{master, 0xf11b5, iteration, slot},
+ * each validity-checked), processes dealt round-robin to the variants, all
+ * (process, component) runs in one launch, prefix sharing for the original,
+ * per-variant component minima.  Requires m_schemes >= 2 (m_schemes = 1 is
+ * plain optimize_scheme) and world = 1. */
+int tcse_optimize_with_flips(tcse_ctx* ctx, const tcse_scheme* scheme, const tcse_search_config* cfg,
+                             const tcse_flip_config* flip, tcse_flip_result* out, tcse_stats* stats);
 
 /* Measured shared-memory word-op peak of this device (roofline
  * denominator): a microbenchmark of the search kernel's inner operation

@@ -323,6 +323,25 @@ int ref_optimize_scheme_json(const char* scheme_json, const tcse_search_config* 
     });
 }
 
+// optimize_with_flips (parallel_search.hpp:354-518) -> report_to_json
+int ref_optimize_with_flips_json(const char* scheme_json, const tcse_search_config* c, int32_t m_schemes,
+                                 int32_t flips_min, int32_t flips_max, uint32_t threads, char* out, int32_t cap,
+                                 int32_t* n_out) {
+    return guarded([&]() -> int {
+        SearchConfig cfg = to_cfg(c, threads);
+        cfg.flip_mode.enabled = true;
+        cfg.flip_mode.m_schemes = m_schemes;
+        cfg.flip_mode.flips_min = flips_min;
+        cfg.flip_mode.flips_max = flips_max;
+        const auto text = report_to_json(optimize_with_flips(parse_scheme(scheme_json), cfg));
+        *n_out = int32_t(text.size());
+        if (int(text.size()) + 1 > cap)
+            return fail(TCSE_ECAPACITY, "report buffer too small");
+        std::memcpy(out, text.c_str(), text.size() + 1);
+        return TCSE_OK;
+    });
+}
+
 // emit_slp (io.hpp:352-393) of a report (parse_report, io.hpp:268-291) for a scheme
 int ref_emit_slp(const char* scheme_json, const char* report_json, char* out, int32_t cap, int32_t* n_out) {
     return guarded([&]() -> int {

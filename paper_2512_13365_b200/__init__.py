@@ -29,6 +29,7 @@ from .slp import combine_componentwise, count_slp_operators, emit_slp, emit_slp_
 __all__ = [
     "TcseError", "LinearSystem", "ProcessConfig", "SearchConfig", "SolutionRecord", "Device",
     "count_pairs", "run_cse", "optimize_system", "optimize_systems", "optimize_scheme", "Search",
+    "optimize_with_flips",
     "verify_record", "report_to_json", "strategy_from_string", "library_path",
     "parse_scheme", "load_scheme", "extract_systems", "naive_cost", "scheme_digest", "verify_brent",
     "SchemeError", "STRATEGY_NAMES", "STRATEGY_SHORT", "DEFAULT_WEIGHTS",
@@ -90,6 +91,8 @@ def lib():
         L.tcse_search_step.argtypes = [C.c_void_p, P(C.c_int32)]
         L.tcse_search_result.argtypes = [C.c_void_p, P(_abi.Record), P(C.c_int32), P(_abi.Stats)]
         L.tcse_search_destroy.argtypes = [C.c_void_p]
+        L.tcse_optimize_with_flips.argtypes = [C.c_void_p, P(_abi.Scheme), P(_abi.SearchConfig), P(_abi.FlipConfig),
+                                               P(_abi.FlipResult), P(_abi.Stats)]
         L.tcse_search_payload_bytes.argtypes = [C.c_void_p]
         L.tcse_search_payload_bytes.restype = C.c_size_t
         L.tcse_search_step_begin.argtypes = [C.c_void_p, C.c_void_p]
@@ -146,16 +149,18 @@ class ProcessConfig(dict):
 
 
 class SearchConfig(dict):
-    """SearchConfig (parallel_search.hpp:44-53) minus flip mode / threads."""
+    """SearchConfig (parallel_search.hpp:44-53) with FlipModeConfig (24-29); no threads knob."""
 
     def __init__(self, n_processes=0, strategy_weights=DEFAULT_WEIGHTS, reinit_fraction=0.40, patience=10,
-                 master_seed=0, forced_strategy=None, max_iterations=0, mix_weights=DEFAULT_MIX):
+                 master_seed=0, forced_strategy=None, max_iterations=0, mix_weights=DEFAULT_MIX,
+                 flip_enabled=False, m_schemes=32, flips_min=1, flips_max=16):
         if isinstance(forced_strategy, str):
             forced_strategy = strategy_from_string(forced_strategy)
         super().__init__(n_processes=n_processes, strategy_weights=tuple(strategy_weights),
                          reinit_fraction=reinit_fraction, patience=patience, master_seed=master_seed,
                          forced_strategy=forced_strategy, max_iterations=max_iterations,
-                         mix_weights=tuple(mix_weights))
+                         mix_weights=tuple(mix_weights), flip_enabled=flip_enabled, m_schemes=m_schemes,
+                         flips_min=flips_min, flips_max=flips_max)
 
     def to_c(self):
         f = self["forced_strategy"]
@@ -506,7 +511,8 @@ def report_to_json(report):
         "strategy_weights": weights,
         "reinit_fraction": _num(cfg["reinit_fraction"]),
         "patience": cfg["patience"],
-        "flip_mode": {"enabled": False, "m_schemes": 32, "flips_min": 1, "flips_max": 16},
+        "flip_mode": {"enabled": bool(cfg.get("flip_enabled", False)), "m_schemes": cfg.get("m_schemes", 32),
+                      "flips_min": cfg.get("flips_min", 1), "flips_max": cfg.get("flips_max", 16)},
         "master_seed": cfg["master_seed"],
     }
     if cfg.get("forced_strategy") is not None:
@@ -522,8 +528,60 @@ def report_to_json(report):
             "seed": rec.seed,
             "iterations": c["iterations"],
         }
+        if report.get("scheme") is not None:
+            comps[key]["scheme_id"] = c.get("scheme_id", "original")
     j = {"scheme_digest": report["scheme_digest"], "config": jc, "components": comps,
          "total": report["total"], "iterations": report["iterations"]}
     if report.get("combined"):
         j["combined"] = True
+    if report.get("scheme") is not None:
+        s = report["scheme"]
+        j["scheme"] = {"m": s["m"], "n": s["n"], "p": s["p"], "r": s["r"], "u": s["u"], "v": s["v"], "w": s["w"]}
     return _dump(j) + "\n"
+
+
+def optimize_with_flips(scheme, cfg, device=None, stats=None):
+    """optimize_with_flips (parallel_search.hpp:354-518): every iteration M
+    random-flip variants of the scheme (slot 0 the input) are searched together
+    on the device; the report carries the winning variant."""
+    cfg = SearchConfig(**cfg)
+    if cfg["m_schemes"] < 1:
+        raise TcseError(_abi.TCSE_EINVAL, "search config: flip mode needs m_schemes >= 1")
+    if cfg["flips_min"] < 1 or cfg["flips_max"] < cfg["flips_min"]:
+        raise TcseError(_abi.TCSE_EINVAL, "search config: flip counts must satisfy 1 <= min <= max")
+    cfg["flip_enabled"] = True
+    if cfg["m_schemes"] == 1:
+        return optimize_scheme(scheme, cfg, device=device, stats=stats)
+    d = device or default_device()
+    m, n, p, r = scheme["m"], scheme["n"], scheme["p"], scheme["r"]
+    flat = lambda t: (C.c_int8 * max(1, sum(len(x) for x in t)))(*[v for row in t for v in row])  # noqa: E731
+    cu, cv, cw = flat(scheme["u"]), flat(scheme["v"]), flat(scheme["w"])
+    cs = _abi.Scheme(m, n, p, r, cu, cv, cw)
+    ou, ov, ow = (C.c_int8 * (r * m * n))(), (C.c_int8 * (r * n * p))(), (C.c_int8 * (m * p * r))()
+    res = _abi.FlipResult()
+    res.u, res.v, res.w = ou, ov, ow
+    cap = r * max(m * n, n * p, m * p) + 1
+    keep = []
+    for k in range(3):
+        rec = make_record(cap)
+        keep.append(rec)
+        res.comp[k] = rec
+    resolved = SearchConfig(**cfg)
+    if resolved["n_processes"] == 0:
+        resolved["n_processes"] = tier_processes(r)
+    fc = _abi.FlipConfig(cfg["m_schemes"], cfg["flips_min"], cfg["flips_max"], 0)
+    st = _abi.Stats()
+    _check(lib().tcse_optimize_with_flips(d.handle, C.byref(cs), C.byref(resolved.to_c()), C.byref(fc),
+                                          C.byref(res), C.byref(st)))
+    if stats is not None:
+        stats.update(_stats_dict(st))
+    carried = dict(m=m, n=n, p=p, r=r, u=[list(ou[q * m * n:(q + 1) * m * n]) for q in range(r)],
+                   v=[list(ov[q * n * p:(q + 1) * n * p]) for q in range(r)],
+                   w=[list(ow[row * r:(row + 1) * r]) for row in range(m * p)])
+    sid = "original" if res.scheme_slot == 0 else "flip-%d-%d" % (res.scheme_iteration, res.scheme_slot)
+    comps = []
+    for k in range(3):
+        rec = SolutionRecord.from_c(res.comp[k])
+        comps.append(dict(record=rec, cost=rec.cost, naive=res.naive[k], iterations=res.iterations, scheme_id=sid))
+    return dict(scheme_digest=scheme_digest(carried), config=resolved, components=comps, total=res.total,
+                iterations=res.iterations, scheme=carried)

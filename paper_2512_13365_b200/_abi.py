@@ -96,6 +96,22 @@ class Stats(C.Structure):
     ]
 
 
+class Scheme(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n", C.c_int32), ("p", C.c_int32), ("r", C.c_int32),
+                ("u", C.POINTER(C.c_int8)), ("v", C.POINTER(C.c_int8)), ("w", C.POINTER(C.c_int8))]
+
+
+class FlipConfig(C.Structure):
+    _fields_ = [("m_schemes", C.c_int32), ("flips_min", C.c_int32), ("flips_max", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class FlipResult(C.Structure):
+    _fields_ = [("u", C.POINTER(C.c_int8)), ("v", C.POINTER(C.c_int8)), ("w", C.POINTER(C.c_int8)),
+                ("comp", Record * 3), ("naive", C.c_int32 * 3), ("iterations", C.c_int32),
+                ("scheme_iteration", C.c_int32), ("scheme_slot", C.c_int32), ("total", C.c_int32)]
+
+
 ITER_CB = C.CFUNCTYPE(C.c_int, C.c_int32, C.c_int32, C.POINTER(Record), C.c_void_p)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 

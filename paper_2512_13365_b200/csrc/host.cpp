@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <random>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -336,6 +338,8 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.sub_cap = d.h.naive / 2 + 1;
     sd.base_masks = d.masks.as<u64>();
     sd.forced = -1;
+    sd.p_stride = 1;
+    sd.stream_comp = -1;
     sd.err = err;
     sd.err_pos = err + 1;
     return sd;
@@ -1340,3 +1344,5 @@ int tcse_verify_record(const tcse_system* sys, const tcse_pair* subs, int32_t n_
 }
 
 }  // extern "C"
+
+#include "flip_mode.inc"

@@ -47,6 +47,8 @@ struct SysDesc {
     int32_t mode;
     int32_t n_local;      // processes of this system in this launch
     int32_t p0;           // global process id of local process 0
+    int32_t p_stride;     // global id of local process lp = p0 + lp * p_stride (flip mode: M)
+    int32_t stream_comp;  // >= 0: process stream = mt19937_64(mix_seed{slot.seed, comp}) (flip mode)
     int32_t block_begin;  // first block of this system
 
     // kModeSearch slot derivation (assign_strategies, parallel_search.hpp:172-208)
@@ -106,6 +108,8 @@ struct LaunchDesc {
     u64* rng;        // [total_blocks][312] seeded mt19937_64 states
     int32_t* perm;   // [total_blocks] launch order -> block (grouped by strategy), or null
     int32_t* hist;   // [kMaxSys][16] strategy histogram + placement cursors
+    const SysDesc* table;  // > kMaxSys systems (flip mode): device table, blocks contiguous per system
+    int32_t table_n;
     SysDesc sys[kMaxSys];
 };
 

@@ -1047,6 +1047,27 @@ struct St {
     int sd_ne;
 };
 
+// the system block `blk` belongs to (blocks are contiguous per system)
+__device__ __forceinline__ const SysDesc& find_sys(const LaunchDesc& L, int blk) {
+    if (L.table) {
+        int lo = 0, hi = L.table_n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (L.table[mid].block_begin <= blk)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        return L.table[lo];
+    }
+    int s = 0;
+#pragma unroll
+    for (int t = 1; t < kMaxSys; ++t)
+        if (t < L.nsys && blk >= L.sys[t].block_begin)
+            s = t;
+    return L.sys[s];
+}
+
 __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) {
     if (atomicCAS(sd.err, 0, code) == 0 && sd.err_pos)
         *sd.err_pos = pos;
@@ -1064,12 +1085,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     // launch order -> process block: blocks of one strategy run together, most
     // expensive strategies first (instruction-cache locality, shorter tail)
     const int blk = L.perm ? L.perm[blockIdx.x] : int(blockIdx.x);
-    int s = 0;
-#pragma unroll
-    for (int t = 1; t < kMaxSys; ++t)
-        if (t < L.nsys && blk >= L.sys[t].block_begin)
-            s = t;
-    const SysDesc& sd = L.sys[s];
+    const SysDesc& sd = find_sys(L, blk);
     const int lp = blk - sd.block_begin;
     if (lp >= sd.n_local)
         return;
@@ -1263,14 +1279,14 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     for (int t = 1; t < kMaxSys; ++t)
         if (t < L.nsys && b >= L.sys[t].block_begin)
             s = t;
-    const SysDesc& sd = L.sys[s];
+    const SysDesc& sd = find_sys(L, b);
     const int lp = b - sd.block_begin;
     if (lp >= sd.n_local)
         return;
     SlotRec r;
     Slot sl;
     if (sd.mode == kModeSearch) {
-        derive_slot(sd, u64(sd.p0 + lp), &sl);
+        derive_slot(sd, u64(sd.p0) + u64(lp) * u64(max(sd.p_stride, 1)), &sl);
         for (int k = 0; k < 4; ++k)
             r.mix[k] = sd.mix[k];
     } else if (sd.mode == kModeRun) {
@@ -1305,8 +1321,16 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     L.slots[b] = r;
     if (L.hist)
         atomicAdd(&L.hist[s * 16 + st], 1);
-    if (rng)
-        mt_seed(L.rng + size_t(b) * 312, sl.seed);
+    if (rng) {
+        // optimize_with_flips seeds each (process, component) stream from
+        // mix_seed{slot.seed, comp} (parallel_search.hpp:441)
+        u64 ps = sl.seed;
+        if (sd.stream_comp >= 0) {
+            ps = splitmix64(0x5851f42d4c957f2dULL ^ ps);
+            ps = splitmix64(ps ^ u64(sd.stream_comp));
+        }
+        mt_seed(L.rng + size_t(b) * 312, ps);
+    }
 }
 
 // launch position of every block: per system, strategies in the order
