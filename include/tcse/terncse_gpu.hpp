@@ -8,6 +8,7 @@
 //   terncse::optimize_scheme   (parallel_search.hpp:314)
 //   terncse::run_cse           (cse_engine.hpp:29), rng = mt19937_64(cfg.seed)
 //   terncse::count_pairs       (linear_system.hpp:151)
+//   terncse::optimize_with_flips (parallel_search.hpp:354)
 //
 // and return the reference's own result types.  Everything around the search
 // stays the reference's code: scheme validation (check_scheme_auto),
@@ -215,6 +216,73 @@ inline SearchReport optimize_scheme(const Scheme& s, const SearchConfig& cfg, Co
         report.total += result.cost;
         report.iterations += result.iterations;
     }
+    report.wall_ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - started)
+                         .count();
+    return report;
+}
+
+// optimize_with_flips (parallel_search.hpp:354-518) with the search on the
+// device; the report carries the winning variant, as the reference's does
+inline SearchReport optimize_with_flips(const Scheme& s, const SearchConfig& cfg, Context& ctx = default_context()) {
+    detail::validate_config(cfg);
+    if (!cfg.flip_mode.enabled)
+        throw error("optimize_with_flips: flip mode is disabled");
+    if (cfg.flip_mode.m_schemes == 1)
+        return gpu::optimize_scheme(s, cfg, ctx);
+    check_structure(s);
+    const auto started = std::chrono::steady_clock::now();
+    SearchConfig resolved = cfg;
+    resolved.n_processes = detail::resolve_processes(cfg, s.r);
+    std::vector<int8_t> u, v, w;
+    for (const auto& row : s.u)
+        u.insert(u.end(), row.begin(), row.end());
+    for (const auto& row : s.v)
+        v.insert(v.end(), row.begin(), row.end());
+    for (const auto& row : s.w)
+        w.insert(w.end(), row.begin(), row.end());
+    const tcse_scheme cs{s.m, s.n, s.p, s.r, u.data(), v.data(), w.data()};
+    std::vector<int8_t> ou(u.size()), ov(v.size()), ow(w.size());
+    const std::size_t cap = std::size_t(s.r) * std::size_t(std::max({s.m * s.n, s.n * s.p, s.m * s.p})) + 1;
+    std::vector<tcse_pair> b0(cap), b1(cap), b2(cap);
+    tcse_flip_result res{};
+    res.u = ou.data();
+    res.v = ov.data();
+    res.w = ow.data();
+    res.comp[0] = {b0.data(), int32_t(cap), 0, 0, 0, 0};
+    res.comp[1] = {b1.data(), int32_t(cap), 0, 0, 0, 0};
+    res.comp[2] = {b2.data(), int32_t(cap), 0, 0, 0, 0};
+    const auto c = detail_gpu::to_c(resolved);
+    const tcse_flip_config fc{cfg.flip_mode.m_schemes, cfg.flip_mode.flips_min, cfg.flip_mode.flips_max, 0};
+    detail_gpu::check(tcse_optimize_with_flips(ctx.get(), &cs, &c, &fc, &res, nullptr));
+    Scheme carried = s;
+    for (int q = 0; q < s.r; ++q) {
+        std::copy_n(ou.data() + std::size_t(q) * std::size_t(s.m * s.n), s.m * s.n, carried.u[std::size_t(q)].begin());
+        std::copy_n(ov.data() + std::size_t(q) * std::size_t(s.n * s.p), s.n * s.p, carried.v[std::size_t(q)].begin());
+    }
+    for (std::size_t row = 0; row < carried.w.size(); ++row)
+        std::copy_n(ow.data() + row * std::size_t(s.r), s.r, carried.w[row].begin());
+    SearchReport report;
+    report.scheme_digest = scheme_digest(carried);
+    report.config = resolved;
+    report.carried_scheme = carried;
+    const std::string id = res.scheme_slot == 0 ? std::string("original")
+                                                : "flip-" + std::to_string(res.scheme_iteration) + "-" +
+                                                      std::to_string(res.scheme_slot);
+    const auto systems = extract_systems(carried);
+    for (std::size_t comp = 0; comp < 3; ++comp) {
+        auto best = detail_gpu::from_c(res.comp[comp]);
+        const auto final_state = replay_prefix(systems[comp], best.substitutions);
+        if (total_cost(final_state) != best.cost || !expand_and_verify(systems[comp], final_state))
+            throw error("optimize_with_flips: internal verification failed");
+        ComponentResult& result = report.components[comp];
+        result.record = std::move(best);
+        result.cost = result.record.cost;
+        result.naive = naive_cost(systems[comp]);
+        result.iterations = res.iterations;
+        result.scheme_id = id;
+        report.total += result.cost;
+    }
+    report.iterations = res.iterations;
     report.wall_ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - started)
                          .count();
     return report;

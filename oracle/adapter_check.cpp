@@ -69,6 +69,19 @@ int main(int argc, char** argv) {
         const auto gpu = report_to_json(gpu::optimize_scheme(s, cfg));
         report(cpu == gpu, std::string("optimize_scheme report bytes: ") + c.name + " n=" + std::to_string(c.n));
     }
+    // 1b. optimize_with_flips (parallel_search.hpp:354-518): byte-identical report
+    for (const Case& c : {Case{"strassen", 9, 2, 3}, Case{"laderman", 32, 2, 5}}) {
+        const Scheme s = parse_scheme(slurp(dir + "/" + c.name + ".json"));
+        SearchConfig cfg;
+        cfg.n_processes = c.n;
+        cfg.patience = c.patience;
+        cfg.master_seed = c.seed;
+        cfg.flip_mode.enabled = true;
+        cfg.flip_mode.m_schemes = 4;
+        const auto cpu = report_to_json(optimize_with_flips(s, cfg));
+        const auto gpu = report_to_json(gpu::optimize_with_flips(s, cfg));
+        report(cpu == gpu, std::string("optimize_with_flips report bytes: ") + c.name);
+    }
     // 2. optimize_system with on_iteration (parallel_search.hpp:220-273)
     std::mt19937_64 gen(1234);
     for (int round = 0; round < 6; ++round) {

@@ -18,4 +18,4 @@ def test_adapter_matches_reference_api():
                        timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "FAIL" not in r.stdout
-    assert r.stdout.count("[PASS]") >= 11
+    assert r.stdout.count("[PASS]") >= 13
