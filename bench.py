@@ -348,6 +348,18 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    # the binding resource is instruction issue, not smem bandwidth: the ncu
+    # capture of the same kernel (committed) gives issue / warp occupancy
+    issue = None
+    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True):
+        if name.endswith("_search_kernel_ncu.json"):
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                nj = json.load(f)
+            pct = lambda k: float(str(nj.get(k, "nan")).split()[0])  # noqa: E731
+            issue = {"issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                     "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                     "source": "profiles/" + name}
+            break
     line = {
         "metric": METRIC, "value": value, "unit": "substitution steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
@@ -357,7 +369,8 @@ def main():
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_gops, "unit": "Gword-ops/s",
                      "frac": achieved / peak_gops if peak_gops else None, "traffic": traffic,
                      "peak_source": "in-repo microbenchmark (tcse_microbench_wordops) on this GPU",
-                     "kernel": "search_kernel<W=1,NT=64>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms)},
+                     "kernel": "search_kernel<W=1,NT=64>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms),
+                     "ncu_issue": issue},
         "clocks": clk,
         "gpu_launches": int(3 * args.steps),  # prep + search + reduce per iteration
         "substitution_steps": int(steps_all),

@@ -84,3 +84,22 @@ def test_optimize_multiword_against_oracle(dev):
         rec, it = T.optimize_system(sys_, cfg, stream_salt=1)
         o = o_optimize_system(sys_, cfg, salt=1)
         assert (rec.substitutions, rec.cost, it) == (o["subs"], o["cost"], o["iterations"])
+
+
+def test_bench_workload_parity_at_scale(dev):
+    """The bench workload itself (S(x)S 4x4x4:49, default mixed weights,
+    reinit 0.4, U/V/W concurrent) at 4096 processes for 2 iterations (the
+    second with prefix sharing) against the oracle: identical incumbents and
+    identical substitution-step counts."""
+    from helpers import fixture_systems
+    systems = fixture_systems("sxs")
+    cfg = T.SearchConfig(n_processes=4096, patience=1 << 20, master_seed=1, max_iterations=2)
+    st = {}
+    got = T.optimize_systems(systems, cfg, [0, 1, 2], stats=st)
+    steps = 0
+    for c, (sys_, (rec, it)) in enumerate(zip(systems, got)):
+        o = o_optimize_system(sys_, cfg, salt=c)
+        assert (rec.substitutions, rec.cost, rec.strategy, rec.seed, it) == (o["subs"], o["cost"], o["strategy"],
+                                                                             o["seed"], o["iterations"])
+        steps += o["steps"]
+    assert st["steps"] == steps
