@@ -39,21 +39,40 @@ METRIC = "CSE substitution steps/sec (1/2/4/8 B200) & best additions at fixed wa
 WORKLOAD = "sxs"
 
 
+# BASELINE.json configs -> (scheme fixture, forced strategy, processes per GPU)
+CONFIGS = {
+    0: ("strassen", "greedy", 16384),
+    1: ("laderman", "greedy_intersections", 4096),
+    2: ("sxs", None, 16384),
+    3: ("naive555_f1000", None, 8192),
+    4: ("sxl", None, 8192),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tcse", choices=["tcse", "reference"])
-    ap.add_argument("--workload", default=WORKLOAD)
-    ap.add_argument("--processes", type=int, default=16384)
+    ap.add_argument("--config", type=int, default=2, choices=range(5),
+                    help="BASELINE.json configs[i]: 0 Strassen forced greedy, 1 Laderman gi, 2 S(x)S mixed "
+                         "(default, the metric's config), 3 5x5x5 stand-in mixed, 4 6x6x6 stand-in mixed")
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--strategy", default=None, help="forced strategy (overrides the config's)")
+    ap.add_argument("--processes", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="payload all-gather transport for --gpus > 1 (gloo stages through host memory; "
                          "lets the multi-rank path run with several ranks on one GPU for testing)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    wl, strat, procs = CONFIGS[args.config]
+    args.workload = args.workload or wl
+    args.strategy = args.strategy or strat
+    args.processes = args.processes or procs
+    return args
 
 
 def load_systems(name):
@@ -63,12 +82,16 @@ def load_systems(name):
 
 
 def config_block(args, world, scaling="weak"):
+    import paper_2512_13365_b200 as T
     s, _ = load_systems(args.workload)
     return {
-        "workload": "%s %dx%dx%d:%d, mixed strategies (reference default weights), reinit 0.4, "
-                    "%d processes/component/GPU, U/V/W concurrent; step = one optimize_system iteration"
-                    % (args.workload, s["m"], s["n"], s["p"], s["r"], args.processes),
-        "scheme_digest": "7da4ac65bf44d830" if args.workload == "sxs" else None,
+        "workload": "%s %dx%dx%d:%d, %s, reinit 0.4, %d processes/component/GPU, U/V/W concurrent; "
+                    "step = one optimize_system iteration"
+                    % (args.workload, s["m"], s["n"], s["p"], s["r"],
+                       "forced %s" % args.strategy if args.strategy else "mixed strategies (reference default weights)",
+                       args.processes),
+        "baseline_config": args.config,
+        "scheme_digest": T.scheme_digest(s),
         "processes_per_gpu": args.processes,
         "processes_total": args.processes * world,
         "master_seed": args.seed,
@@ -148,9 +171,11 @@ def run_reference(args, rank, world):
     # the GPU arm runs processes x gpus per component; the CPU's steps/s does
     # not depend on the process count once it exceeds the thread count, so the
     # reference is sampled at up to 16384 processes to bound its run time
-    n_proc = min(args.processes * args.gpus, 16384)
+    scheme, _ = load_systems(args.workload)
+    n_proc = min(args.processes * args.gpus, 16384 if scheme["r"] < 100 else 512)
     its = args.warmup + args.steps
-    cfg = T.SearchConfig(n_processes=n_proc, patience=1 << 30, master_seed=args.seed, max_iterations=its).to_c()
+    cfg = T.SearchConfig(n_processes=n_proc, patience=1 << 30, master_seed=args.seed, max_iterations=its,
+                         forced_strategy=args.strategy).to_c()
     secs = steps = 0.0
     for comp, (nx, rows) in enumerate(systems):
         s = _abi.make_system(nx, rows)
@@ -164,7 +189,7 @@ def run_reference(args, rank, world):
             raise RuntimeError(ref.ref_last_error().decode())
         secs += sum(isecs[args.warmup:its])
         steps += sum(isteps[args.warmup:its])
-    value = steps / secs
+    value = steps / secs if secs > 0 else 0.0
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "substitution steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -190,9 +215,11 @@ def cpu_baseline_sample(args):
     from paper_2512_13365_b200 import _abi
     ref = reference()
     threads = os.cpu_count() or 1
-    _, systems = load_systems(args.workload)
-    cfg = T.SearchConfig(n_processes=args.processes, patience=1 << 30, master_seed=args.seed,
-                         max_iterations=1).to_c()
+    scheme, systems = load_systems(args.workload)
+    # bounded sample (~seconds): large schemes cost far more per process on the CPU
+    n_cpu = min(args.processes, 16384 if scheme["r"] < 100 else 512)
+    cfg = T.SearchConfig(n_processes=n_cpu, patience=1 << 30, master_seed=args.seed,
+                         max_iterations=1, forced_strategy=args.strategy).to_c()
     secs = steps = 0.0
     for comp, (nx, rows) in enumerate(systems):
         s = _abi.make_system(nx, rows)
@@ -204,10 +231,11 @@ def cpu_baseline_sample(args):
             raise RuntimeError(ref.ref_last_error().decode())
         secs += tot.value
         steps += st.value
-    return {"value": steps / secs, "unit": "substitution steps/s", "cores": threads, "kind": "reference",
+    return {"value": steps / secs if secs > 0 else 0.0, "unit": "substitution steps/s", "cores": threads,
+            "kind": "reference",
             "sample": "iteration 1 of optimize_system on U, V, W (%d processes each, %.0f steps, %.1f s), "
                       "threads=%d, oracle/_ref built from the reference headers with its Release flags"
-                      % (args.processes, steps, secs, threads)}
+                      % (n_cpu, steps, secs, threads)}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -266,7 +294,7 @@ def main():
     _, sys_rows = load_systems(args.workload)
     systems = [T.LinearSystem(nx, rows) for nx, rows in sys_rows]
     n_total = args.processes * world
-    cfg = T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed)
+    cfg = T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed, forced_strategy=args.strategy)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     search = T.Search(systems, cfg, [0, 1, 2], device=dev)
@@ -307,7 +335,8 @@ def main():
         # the public session API: host CSR in (create uploads the systems),
         # K iterations, host records out
         s2 = T.Search(systems, T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed,
-                                              max_iterations=args.steps), [0, 1, 2], device=dev)
+                                              max_iterations=args.steps, forced_strategy=args.strategy),
+                      [0, 1, 2], device=dev)
         while step(s2) > 0:
             pass
         _, st = s2.result()

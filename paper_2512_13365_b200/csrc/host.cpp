@@ -25,7 +25,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "launch.h"
@@ -86,7 +88,51 @@ int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
-// device buffer that grows, never shrinks
+// Process-wide caching allocator: every C-ABI call is synchronous, so a
+// buffer released by a finished call can be reused by the next one without
+// the cost (and implicit device synchronisation) of cudaFree/cudaMalloc.
+// Power-of-two buckets per device; memory is retained until process exit.
+struct DeviceCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void*> free_blocks;
+};
+
+DeviceCache& device_cache() {
+    static DeviceCache* c = new DeviceCache;  // never destroyed: outlives static DBufs
+    return *c;
+}
+
+size_t bucket_bytes(size_t bytes) {
+    size_t b = 256;
+    while (b < bytes)
+        b <<= 1;
+    return b;
+}
+
+cudaError_t cache_get(size_t bytes, void** p) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t b = bucket_bytes(bytes);
+    {
+        std::lock_guard<std::mutex> lock(device_cache().mu);
+        auto it = device_cache().free_blocks.find({dev, b});
+        if (it != device_cache().free_blocks.end()) {
+            *p = it->second;
+            device_cache().free_blocks.erase(it);
+            return cudaSuccess;
+        }
+    }
+    return cudaMalloc(p, b);
+}
+
+void cache_put(void* p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(device_cache().mu);
+    device_cache().free_blocks.insert({{dev, bucket_bytes(bytes)}, p});
+}
+
+// device buffer that grows, never shrinks (storage from the cache above)
 struct DBuf {
     void* p = nullptr;
     size_t n = 0;
@@ -97,17 +143,17 @@ struct DBuf {
         if (bytes <= n)
             return cudaSuccess;
         if (p)
-            cudaFree(p);
+            cache_put(p, n);
         p = nullptr;
         n = 0;
-        cudaError_t e = cudaMalloc(&p, bytes);
+        cudaError_t e = cache_get(bytes, &p);
         if (e == cudaSuccess)
-            n = bytes;
+            n = bucket_bytes(bytes);
         return e;
     }
     ~DBuf() {
         if (p)
-            cudaFree(p);
+            cache_put(p, n);
     }
     template <typename T>
     T* as() const {
