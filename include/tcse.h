@@ -134,6 +134,19 @@ typedef struct tcse_scheme {
     const int8_t* w;
 } tcse_scheme;
 
+/* CheckMethod (scheme.hpp:29); TCSE_CHECK_AUTO = check_scheme_auto's rule
+ * (parallel_search.hpp:296-302: rank >= 200 -> randomized product check) */
+enum { TCSE_CHECK_AUTO = -1, TCSE_CHECK_BRENT = 0, TCSE_CHECK_PRODUCT = 1 };
+
+/* SchemeCheckReport (scheme.hpp:31-35); first_violation is "" when valid,
+ * else the reference's wording: "brent(i,j,k,l,i2,j2)" or
+ * "trial T mismatch at c[i][j]". */
+typedef struct tcse_check_report {
+    int32_t valid;
+    int32_t method; /* TCSE_CHECK_BRENT or TCSE_CHECK_PRODUCT */
+    char first_violation[64];
+} tcse_check_report;
+
 /* FlipModeConfig (parallel_search.hpp:24-29) */
 typedef struct tcse_flip_config {
     int32_t m_schemes;
@@ -297,6 +310,19 @@ int tcse_optimize_with_flips(tcse_ctx* ctx, const tcse_scheme* scheme, const tcs
  * denominator): a microbenchmark of the search kernel's inner operation
  * (two 8-byte LDS, AND, POPC, accumulate) over every SM.  *gops = Gword-ops/s. */
 int tcse_microbench_wordops(tcse_ctx* ctx, double* gops);
+
+/* Batched scheme verification on the device: for every
+ * scheme, check_structure (scheme.hpp:54-62; ternary coefficients, positive
+ * dimensions) then verify_brent (scheme.hpp:68-95: every Brent identity,
+ * exact integers, first violation in (i,j,k,l,i2,j2) order) or
+ * verify_by_product (scheme.hpp:99-137: `trials` random integer products,
+ * entries uniform_int(-8,8) from mt19937_64(seed), first mismatch in
+ * (trial,i,j) order) as `method` says; TCSE_CHECK_AUTO picks per scheme like
+ * check_scheme_auto.  Reports are identical to the reference's.  Errors:
+ * TCSE_EINVAL with check_structure's message ("scheme: ...") for the first
+ * malformed scheme, or "verify_by_product: trials must be >= 1". */
+int tcse_verify_schemes(tcse_ctx* ctx, const tcse_scheme* schemes, int32_t count, int32_t method,
+                        int32_t trials, uint64_t seed, tcse_check_report* out);
 
 /* Host-side result/verification API kept from the reference (no GPU):
  * replay_prefix + total_cost + expand_and_verify (linear_system.hpp:193-258,

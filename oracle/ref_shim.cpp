@@ -396,4 +396,39 @@ int ref_flipped_naive_json(int32_t m, int32_t n, int32_t p, int32_t flips, uint6
     });
 }
 
+// verify_brent / verify_by_product / check_scheme_auto (scheme.hpp:68-137,
+// parallel_search.hpp:296-302) of a flat scheme; structural errors come back
+// as TCSE_EINVAL with the reference's message.
+int ref_check_scheme(const tcse_scheme* c, int32_t method, int32_t trials, uint64_t seed, tcse_check_report* out) {
+    return guarded([&]() -> int {
+        Scheme s;
+        s.m = c->m;
+        s.n = c->n;
+        s.p = c->p;
+        s.r = c->r;
+        const std::size_t mn = std::size_t(c->m) * c->n, np = std::size_t(c->n) * c->p, mp = std::size_t(c->m) * c->p;
+        if (c->r > 0 && c->m > 0 && c->n > 0 && c->p > 0) {
+            for (int q = 0; q < c->r; ++q) {
+                s.u.emplace_back(c->u + q * mn, c->u + (q + 1) * mn);
+                s.v.emplace_back(c->v + q * np, c->v + (q + 1) * np);
+            }
+            for (std::size_t row = 0; row < mp; ++row)
+                s.w.emplace_back(c->w + row * c->r, c->w + (row + 1) * c->r);
+        }
+        SchemeCheckReport rep;
+        if (method == TCSE_CHECK_BRENT)
+            rep = verify_brent(s);
+        else if (method == TCSE_CHECK_PRODUCT)
+            rep = verify_by_product(s, trials, seed);
+        else
+            rep = detail::check_scheme_auto(s, seed);
+        std::memset(out, 0, sizeof *out);
+        out->valid = rep.valid ? 1 : 0;
+        out->method = rep.method == CheckMethod::exact_brent ? TCSE_CHECK_BRENT : TCSE_CHECK_PRODUCT;
+        if (rep.first_violation)
+            std::snprintf(out->first_violation, sizeof out->first_violation, "%s", rep.first_violation->c_str());
+        return TCSE_OK;
+    });
+}
+
 }  // extern "C"

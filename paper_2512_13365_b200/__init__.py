@@ -37,7 +37,9 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libtcse.so")
+# TCSE_LIBRARY: load another build of the same ABI (A/B timing of kernel
+# variants, scripts/ab_build.sh); default is the in-tree product library
+_LIB_PATH = os.environ.get("TCSE_LIBRARY") or os.path.join(HERE, "libtcse.so")
 _lib_lock = threading.Lock()
 _lib = None
 
@@ -93,6 +95,8 @@ def lib():
         L.tcse_search_destroy.argtypes = [C.c_void_p]
         L.tcse_optimize_with_flips.argtypes = [C.c_void_p, P(_abi.Scheme), P(_abi.SearchConfig), P(_abi.FlipConfig),
                                                P(_abi.FlipResult), P(_abi.Stats)]
+        L.tcse_verify_schemes.argtypes = [C.c_void_p, P(_abi.Scheme), C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                          P(_abi.CheckReport)]
         L.tcse_search_payload_bytes.argtypes = [C.c_void_p]
         L.tcse_search_payload_bytes.restype = C.c_size_t
         L.tcse_search_step_begin.argtypes = [C.c_void_p, C.c_void_p]
@@ -585,3 +589,73 @@ def optimize_with_flips(scheme, cfg, device=None, stats=None):
         comps.append(dict(record=rec, cost=rec.cost, naive=res.naive[k], iterations=res.iterations, scheme_id=sid))
     return dict(scheme_digest=scheme_digest(carried), config=resolved, components=comps, total=res.total,
                 iterations=res.iterations, scheme=carried)
+
+
+CHECK_METHODS = {"auto": _abi.TCSE_CHECK_AUTO, "exact_brent": _abi.TCSE_CHECK_BRENT,
+                 "randomized_product": _abi.TCSE_CHECK_PRODUCT}
+
+
+class CheckReport(tuple):
+    """SchemeCheckReport (scheme.hpp:31-35): (valid, first_violation or None,
+    method "exact_brent" | "randomized_product")."""
+    __slots__ = ()
+
+    def __new__(cls, valid, first_violation, method):
+        return tuple.__new__(cls, (valid, first_violation, method))
+
+    valid = property(lambda self: self[0])
+    first_violation = property(lambda self: self[1])
+    method = property(lambda self: self[2])
+
+
+def _check_tensor_shape(t, name, rows, cols):
+    """detail::check_tensor's shape messages (scheme.hpp:39-52); the
+    coefficient range is checked by the library with the same words."""
+    if len(t) != rows:
+        raise TcseError(_abi.TCSE_EINVAL, "scheme: tensor %s has %d rows, expected %d" % (name, len(t), rows))
+    for row, entries in enumerate(t):
+        if len(entries) != cols:
+            raise TcseError(_abi.TCSE_EINVAL, "scheme: tensor %s row %d has %d entries, expected %d"
+                            % (name, row, len(entries), cols))
+
+
+def verify_schemes(schemes, method="auto", trials=16, seed=0, device=None):
+    """Batched device check of scheme dicts (one launch): verify_brent
+    (scheme.hpp:68-95), verify_by_product (99-137) or check_scheme_auto's
+    rule (parallel_search.hpp:296-302) per scheme.  Raises TcseError with
+    check_structure's message on a malformed scheme."""
+    if method not in CHECK_METHODS:
+        raise ValueError("method must be one of %s" % sorted(CHECK_METHODS))
+    if not schemes:
+        return []
+    for s in schemes:  # shapes first: a flat C array cannot be ragged
+        m, n, p, r = s["m"], s["n"], s["p"], s["r"]
+        if m < 1 or n < 1 or p < 1 or r < 1:
+            raise TcseError(_abi.TCSE_EINVAL, "scheme: dimensions and rank must be positive")
+        _check_tensor_shape(s["u"], "u", r, m * n)
+        _check_tensor_shape(s["v"], "v", r, n * p)
+        _check_tensor_shape(s["w"], "w", m * p, r)
+    d = device or default_device()
+    cs = (_abi.Scheme * len(schemes))()
+    keep = []
+    for t, s in enumerate(schemes):
+        m, n, p, r = s["m"], s["n"], s["p"], s["r"]
+        flat = [(C.c_int8 * max(1, len(x) * len(x[0])))(*[max(-128, min(127, v)) for row in x for v in row])
+                for x in (s["u"], s["v"], s["w"])]
+        keep.append(flat)
+        cs[t] = _abi.Scheme(m, n, p, r, *flat)
+    out = (_abi.CheckReport * len(schemes))()
+    _check(lib().tcse_verify_schemes(d.handle, cs, len(schemes), CHECK_METHODS[method], trials, seed, out))
+    names = {_abi.TCSE_CHECK_BRENT: "exact_brent", _abi.TCSE_CHECK_PRODUCT: "randomized_product"}
+    return [CheckReport(bool(o.valid), o.first_violation.decode() if not o.valid else None, names[o.method])
+            for o in out]
+
+
+def verify_brent_device(scheme, device=None):
+    """verify_brent (scheme.hpp:68-95) of one scheme on the device."""
+    return verify_schemes([scheme], "exact_brent", device=device)[0]
+
+
+def verify_by_product_device(scheme, trials, seed, device=None):
+    """verify_by_product (scheme.hpp:99-137) of one scheme on the device."""
+    return verify_schemes([scheme], "randomized_product", trials, seed, device=device)[0]

@@ -101,6 +101,13 @@ class Scheme(C.Structure):
                 ("u", C.POINTER(C.c_int8)), ("v", C.POINTER(C.c_int8)), ("w", C.POINTER(C.c_int8))]
 
 
+TCSE_CHECK_AUTO, TCSE_CHECK_BRENT, TCSE_CHECK_PRODUCT = -1, 0, 1
+
+
+class CheckReport(C.Structure):
+    _fields_ = [("valid", C.c_int32), ("method", C.c_int32), ("first_violation", C.c_char * 64)]
+
+
 class FlipConfig(C.Structure):
     _fields_ = [("m_schemes", C.c_int32), ("flips_min", C.c_int32), ("flips_max", C.c_int32),
                 ("reserved", C.c_int32)]

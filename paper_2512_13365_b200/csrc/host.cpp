@@ -38,6 +38,15 @@ struct ReduceLaunch;
 }  // namespace tcse
 
 namespace tcse {
+struct VerifyDesc {  // verify.cu
+    int32_t m, n, p, r;
+    int32_t method;
+    int32_t trials;
+    int64_t off_u, off_v, off_w, off_ab;
+    int64_t n_checks;
+};
+cudaError_t launch_verify(const VerifyDesc* d_descs, const int8_t* d_coef, unsigned long long* d_first, int count,
+                          long long max_checks, int max_trials, int max_r, int n_sms, cudaStream_t st);
 cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st);
 cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st);
 }  // namespace tcse

@@ -105,3 +105,21 @@ def o_sequence_fnv(subs):
 
 def _naive(sys):
     return sum(len(r) - 1 for r in sys[1] if r)
+
+
+CHECK_METHOD = {"auto": -1, "exact_brent": 0, "randomized_product": 1}
+
+
+def ref_check_scheme(s, method="auto", trials=16, seed=0):
+    """The reference's verify_brent / verify_by_product / check_scheme_auto
+    -> (valid, first_violation or None, method name); raises ValueError with
+    the reference's message on a structural error."""
+    flat = [(C.c_int8 * max(1, sum(len(r) for r in x)))(*[v for row in x for v in row]) for x in (s["u"], s["v"], s["w"])]
+    cs = _abi.Scheme(s["m"], s["n"], s["p"], s["r"], *flat)
+    out = _abi.CheckReport()
+    lib = reference()
+    rc = lib.ref_check_scheme(C.byref(cs), CHECK_METHOD[method], trials, seed, C.byref(out))
+    if rc != 0:
+        raise ValueError(lib.ref_last_error().decode())
+    name = "exact_brent" if out.method == 0 else "randomized_product"
+    return (bool(out.valid), None if out.valid else out.first_violation.decode(), name)

@@ -9,8 +9,8 @@ import functools
 import os
 import subprocess
 
-from paper_2512_13365_b200._abi import (Pair, PairCount, ProcessConfig, Record, SearchConfig,
-                                        System)
+from paper_2512_13365_b200._abi import (CheckReport, Pair, PairCount, ProcessConfig, Record, Scheme,
+                                        SearchConfig, System)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_DIR = os.path.join(ROOT, "oracle")
@@ -74,6 +74,7 @@ def reference():
     lib.ref_scheme_info.argtypes = [C.c_char_p, C.c_char_p, P(C.c_int32), P(C.c_int32)]
     lib.ref_optimize_scheme_json.argtypes = [C.c_char_p, P(SearchConfig), C.c_uint32, C.c_char_p,
                                              C.c_int32, P(C.c_int32)]
+    lib.ref_check_scheme.argtypes = [P(Scheme), C.c_int32, C.c_int32, C.c_uint64, P(CheckReport)]
     lib.ref_flipped_naive_json.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
                                            C.c_char_p, C.c_int32, P(C.c_int32)]
     return lib
