@@ -95,8 +95,9 @@ def lib():
         L.tcse_search_destroy.argtypes = [C.c_void_p]
         L.tcse_optimize_with_flips.argtypes = [C.c_void_p, P(_abi.Scheme), P(_abi.SearchConfig), P(_abi.FlipConfig),
                                                P(_abi.FlipResult), P(_abi.Stats)]
-        L.tcse_verify_schemes.argtypes = [C.c_void_p, P(_abi.Scheme), C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
-                                          P(_abi.CheckReport)]
+        if hasattr(L, "tcse_verify_schemes") or not os.environ.get("TCSE_LIBRARY"):  # older A/B builds lack it
+            L.tcse_verify_schemes.argtypes = [C.c_void_p, P(_abi.Scheme), C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_uint64, P(_abi.CheckReport)]
         L.tcse_search_payload_bytes.argtypes = [C.c_void_p]
         L.tcse_search_payload_bytes.restype = C.c_size_t
         L.tcse_search_step_begin.argtypes = [C.c_void_p, C.c_void_p]

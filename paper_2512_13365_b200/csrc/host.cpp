@@ -449,6 +449,11 @@ int base_candidates(tcse_ctx* ctx, DevSys& d) {
     if (n > d.h.mcap)
         return fail(TCSE_ECAPACITY, "candidate capacity %d < %d", d.h.mcap, n);
     d.base_m = n;
+    // gi form on the actual starting list (lists only shrink): the dense
+    // reference loop up to ~1k candidates, the O(deg) walk beyond (A/B on
+    // every fixture)
+    if (env_int("TCSE_GI_DENSE", -1) < 0)
+        d.dense = n <= 1024;
     return TCSE_OK;
 }
 
