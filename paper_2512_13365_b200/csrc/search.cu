@@ -177,7 +177,14 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* red) {
     return r;
 }
 
-// first maximum of (score, index): larger score wins, ties to smaller index
+// (s2, i2) beats (s, i): a thread without a candidate (index 0x7fffffff)
+// always loses — scores can be negative for user alpha/beta — otherwise the
+// higher score, ties to the lower index (the reference's strict-> first max)
+__device__ __forceinline__ bool argmax_better(double s2, int i2, double s, int i) {
+    return i2 != 0x7fffffff && (i == 0x7fffffff || s2 > s || (s2 == s && i2 < i));
+}
+
+// first maximum of (score, index) over the block
 template <int NT>
 __device__ __forceinline__ int block_argmax_double(double s, int idx, double* reds, int* redi) {
     constexpr int NW = NT / 32;
@@ -185,7 +192,7 @@ __device__ __forceinline__ int block_argmax_double(double s, int idx, double* re
     for (int o = 16; o > 0; o >>= 1) {
         const double s2 = __shfl_down_sync(FULLMASK, s, o);
         const int i2 = __shfl_down_sync(FULLMASK, idx, o);
-        if (s2 > s || (s2 == s && i2 < idx)) {
+        if (argmax_better(s2, i2, s, idx)) {
             s = s2;
             idx = i2;
         }
@@ -201,7 +208,7 @@ __device__ __forceinline__ int block_argmax_double(double s, int idx, double* re
     int bi = redi[0];
 #pragma unroll
     for (int w = 1; w < NW; ++w)
-        if (reds[w] > bs || (reds[w] == bs && redi[w] < bi)) {
+        if (argmax_better(reds[w], redi[w], bs, bi)) {
             bs = reds[w];
             bi = redi[w];
         }
@@ -707,6 +714,10 @@ struct St {
     // evaluated in O(deg q) (see the header comment).
     template <bool dense>
     __device__ int sel_gi(double alpha, double beta) {
+        // the walk needs a non-decreasing running sum (beta >= 0, always true
+        // for assign_strategies' slots); any other beta runs the reference loop
+        const bool walk = !dense && beta >= 0.0;
+        __shared__ u32 s_wmax;  // max c - 1 over the list (walk: crossing bound)
         const u32* ks = keys();
         const u16* c = cnts();
         const int V1 = V + 1;
@@ -717,15 +728,17 @@ struct St {
         const u32* coin = sp<u32>(lay.coin);
         for (int v = tid; v < V1; v += NT) {
             nA[v] = 0u;
-            if (!dense)
+            if (walk)
                 nB[v] = 0u;
         }
         for (int cc = tid; cc <= sd_ne; cc += NT)
             wbt[cc] = __dmul_rn(beta, double(cc - 1));
+        if (tid == 0)
+            s_wmax = 0u;
         __syncthreads();
-        // per-variable candidate counts (dense: total in nA; walk: A = as
+        // per-variable candidate counts (reference loop: total in nA; walk: A = as
         // second element, B = as first element)
-        if (dense) {
+        if (!walk) {
             for (int t = tid; t < m; t += NT) {
                 const u32 kk = ks[t];
                 atomicAdd(&nA[key_i(kk)], 1u);
@@ -733,6 +746,7 @@ struct St {
             }
         } else {
             u32* bs = sp<u32>(lay.bs);
+            u32 lmax = 0u;
             for (int t = tid; t < m; t += NT) {
                 const u32 kk = ks[t];
                 const int a = key_i(kk), b = key_j(kk);
@@ -740,10 +754,14 @@ struct St {
                 atomicAdd(&nB[a], 1u);
                 if (t == 0 || key_i(ks[t - 1]) != a)
                     bs[a] = u32(t);
+                lmax = max(lmax, u32(c[t]) - 1u);
             }
+            lmax = __reduce_max_sync(FULLMASK, lmax);
+            if (lane == 0)
+                atomicMax(&s_wmax, lmax);
         }
         __syncthreads();
-        if (!dense) {
+        if (walk) {
             // A-list offsets: scan over variables
             u32* aoff = sp<u32>(lay.aoff);
             u32* cursor = sp<u32>(lay.cursor);
@@ -774,12 +792,12 @@ struct St {
                                      ? 1u
                                      : 0u;
                 const int a = key_i(kk), b = key_j(kk);
-                ld += dense ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
+                ld += !walk ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
                 lw += u32(c[e]) - 1u;
             }
             u32 exd = block_scan<NT>(ld, red(), &D);
             u32 W_ = 0, exw = 0;
-            if (!dense)
+            if (walk)
                 exw = block_scan<NT>(lw, red(), &W_);
             u32* wp = sp<u32>(lay.wp);
             for (int e = e0; e < e1; ++e) {
@@ -790,15 +808,15 @@ struct St {
                                      : 0u;
                 const int a = key_i(kk), b = key_j(kk);
                 qbase[e] = exd;
-                exd += dense ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
-                if (!dense) {
+                exd += !walk ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
+                if (walk) {
                     wp[e] = exw;
                     exw += u32(c[e]) - 1u;
                 }
             }
             if (tid == 0) {
                 qbase[m] = D;
-                if (!dense)
+                if (walk)
                     wp[m] = W_;
             }
         }
@@ -806,7 +824,8 @@ struct St {
         last_coins = D;
         double best_s = -1.0;
         int best_q = 0x7fffffff;
-        if (!dense) {
+        const double topmin = double(s_wmax) + 1.0;
+        if (walk) {
             u32* aoff = sp<u32>(lay.aoff);
             u32* cursor = sp<u32>(lay.cursor);
             u32* bs = sp<u32>(lay.bs);
@@ -858,7 +877,7 @@ struct St {
                         const int s = min(xi, xj);
                         pi += xi == s;
                         pj += xj == s;
-                        f = add_run(f, prev, s == 0x7fffffff ? m : s, wp);
+                        f = add_run(f, prev, s == 0x7fffffff ? m : s, wp, topmin);
                         if (s == 0x7fffffff)
                             break;
                         prev = s + 1;
@@ -945,12 +964,17 @@ struct St {
     }
 
     // Sequential double sum f + w_L + ... + w_{R-1} (w_t = c_t - 1 >= 1,
-    // wp = exclusive prefix sums), bit-identical to adding one at a time:
-    // integer additions are exact until the running sum crosses a binade
-    // (sums stay far below 2^53), where exactly one rounding happens.
-    __device__ __forceinline__ double add_run(double f, int L, int R, const u32* wp) {
-        while (L < R) {
-            const u32 tot = wp[R] - wp[L];
+    // wp = exclusive prefix sums, f >= 0), bit-identical to adding one at a
+    // time: integer additions are exact until the running sum crosses a
+    // binade, where exactly one rounding happens.  Integers never change the
+    // fraction of f and below 2^52 the tie bit is fractional, so the rounding
+    // at a crossing depends only on the fraction and the new binade — not on
+    // which element crosses — as long as no single element can skip a binade
+    // (top >= topmin = max w + 1): then the crossing is done in O(1).  Below
+    // that the crossing element is located by binary search in wp.
+    __device__ __forceinline__ double add_run(double f, int L, int R, const u32* wp, double topmin) {
+        u32 tot = wp[R] - wp[L];
+        while (tot != 0u) {
             if (f == trunc(f))
                 return __dadd_rn(f, double(tot));  // integer + integer: exact
             const long long bits = __double_as_longlong(f);
@@ -958,18 +982,25 @@ struct St {
             const double gap = __dsub_rn(top, f);  // exact (Sterbenz)
             if (double(tot) < gap)
                 return __dadd_rn(f, double(tot));  // stays in the binade: exact
-            // first element whose partial sum reaches the binade top
-            const u32 need = wp[L] + u32(ceil(gap));
-            int lo = L + 1, hi = R;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (wp[mid] >= need)
-                    hi = mid;
-                else
-                    lo = mid + 1;
+            u32 step;
+            if (top >= topmin) {
+                step = u32(ceil(gap));  // any crossing partial sum rounds alike
+            } else {
+                // first element whose partial sum reaches the binade top
+                const u32 need = wp[L] + u32(ceil(gap));
+                int lo = L + 1, hi = R;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (wp[mid] >= need)
+                        hi = mid;
+                    else
+                        lo = mid + 1;
+                }
+                step = wp[lo] - wp[L];
+                L = lo;
             }
-            f = __dadd_rn(f, double(wp[lo] - wp[L]));  // the one rounding
-            L = lo;
+            f = __dadd_rn(f, double(step));  // the one rounding
+            tot -= step;
         }
         return f;
     }

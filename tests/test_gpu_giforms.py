@@ -1,0 +1,82 @@
+"""Both exact Greedy-Intersections forms against the oracle (search.cu
+sel_gi / add_run): the dense reference loop (TCSE_GI_DENSE=1) and the O(deg)
+walk (TCSE_GI_DENSE=0), forced on the same processes.
+
+The walk adds runs of disjoint candidates in O(1), including the binade
+crossings of the running double sum: by binary search below max(c-1)+1 and
+in closed form above it.  The cases below push both regimes: high pair counts
+(tall systems: many expressions over few variables, so c-1 is large and the
+sum crosses many binades), betas whose products have full 52-bit fractions,
+beta = 0 (integer sums), beta > 1, tiny beta, and negative beta (the walk
+layout then runs the reference loop); negative alpha (every score below -1:
+the block argmax must still return a real candidate, as the reference's
+first-candidate rule does — for gp too).  Records and per-step candidate-list
+traces must equal the oracle's in every case."""
+import random
+
+import pytest
+
+import paper_2512_13365_b200 as T
+from helpers import fixture_systems, o_optimize_system, o_run_cse, random_system
+
+pytestmark = pytest.mark.gpu
+
+BETAS = [0.5, 0.75, 0.6180339887498949, 1.0, 0.0, 3.7, 1e-300, 0.9999999999999999, -0.6]
+
+
+def tall_system(rng, n_e, n_x, density):
+    rows = []
+    for _ in range(n_e):
+        rows.append([v if rng.random() < 0.5 else -v for v in range(1, n_x + 1) if rng.random() < density])
+    return n_x, rows
+
+
+def gi_cfgs(rng, n):
+    out = []
+    for t in range(n):
+        beta = BETAS[t % len(BETAS)] if t < len(BETAS) else 0.5 + rng.random() * 0.5
+        strategy = 4 if t % 3 else 5  # gi, and mixed (which draws gi among others)
+        out.append(T.ProcessConfig(strategy, alpha=rng.choice([0.05, 0.3, 0.5, 1.7, -0.4, -3.0]), beta=beta,
+                                   p_greedy=0.5 + rng.random() * 0.5, seed=rng.getrandbits(64)))
+    return out
+
+
+def systems(rng):
+    out = [random_system(rng, 40, 12) for _ in range(4)]
+    out += [tall_system(rng, 90, 8, 0.45), tall_system(rng, 200, 9, 0.35), tall_system(rng, 250, 14, 0.2)]
+    out += [fixture_systems("sxs")[2], fixture_systems("naive555_f1000")[2]]
+    return out
+
+
+@pytest.mark.parametrize("form", ["1", "0"])
+def test_gi_forms_match_oracle(dev, monkeypatch, form):
+    monkeypatch.setenv("TCSE_GI_DENSE", form)
+    rng = random.Random(4242)
+    for sys_ in systems(rng):
+        cfgs = gi_cfgs(rng, 18)
+        recs, traces = T.run_cse(sys_, cfgs, trace_stride=32)
+        for cfg, rec, tr in zip(cfgs, recs, traces):
+            subs, cost, otr = o_run_cse(sys_, cfg, trace_cap=32)
+            assert (rec.substitutions, rec.cost) == (subs, cost), (form, cfg)
+            assert tr == otr, (form, cfg)
+
+
+@pytest.mark.parametrize("form", ["1", "0"])
+def test_gi_forms_optimize_system(dev, monkeypatch, form):
+    monkeypatch.setenv("TCSE_GI_DENSE", form)
+    rng = random.Random(99)
+    for sys_ in (tall_system(rng, 160, 10, 0.3), fixture_systems("naive555_f1000")[2]):
+        cfg = T.SearchConfig(n_processes=96, patience=3, master_seed=5, forced_strategy=4)
+        st = {}
+        rec, it = T.optimize_system(sys_, cfg, stats=st)
+        o = o_optimize_system(sys_, cfg)
+        assert (rec.substitutions, rec.cost, it, st["steps"]) == (o["subs"], o["cost"], o["iterations"], o["steps"])
+
+
+def test_negative_scores_gp(dev):
+    rng = random.Random(31)
+    for _ in range(6):
+        sys_ = random_system(rng, 30, 10)
+        cfgs = [T.ProcessConfig(6, alpha=rng.choice([-0.5, -2.0, -7.5]), seed=rng.getrandbits(64)) for _ in range(8)]
+        for cfg, rec in zip(cfgs, T.run_cse(sys_, cfgs)):
+            assert (rec.substitutions, rec.cost) == o_run_cse(sys_, cfg), cfg
