@@ -450,10 +450,11 @@ int base_candidates(tcse_ctx* ctx, DevSys& d) {
         return fail(TCSE_ECAPACITY, "candidate capacity %d < %d", d.h.mcap, n);
     d.base_m = n;
     // gi form on the actual starting list (lists only shrink): the dense
-    // reference loop up to ~1k candidates, the O(deg) walk beyond (A/B on
+    // reference loop up to 512 candidates, the O(deg) walk beyond (sweep on
     // every fixture)
+    static const int dense_max = env_int("TCSE_GI_DENSE_MAX", 512);
     if (env_int("TCSE_GI_DENSE", -1) < 0)
-        d.dense = n <= 1024;
+        d.dense = n <= dense_max;
     return TCSE_OK;
 }
 

@@ -177,14 +177,10 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* red) {
     return r;
 }
 
-// (s2, i2) beats (s, i): a thread without a candidate (index 0x7fffffff)
-// always loses — scores can be negative for user alpha/beta — otherwise the
-// higher score, ties to the lower index (the reference's strict-> first max)
-__device__ __forceinline__ bool argmax_better(double s2, int i2, double s, int i) {
-    return i2 != 0x7fffffff && (i == 0x7fffffff || s2 > s || (s2 == s && i2 < i));
-}
-
-// first maximum of (score, index) over the block
+// first maximum of (score, index): larger score wins, ties to the smaller
+// index (the reference's strict-> scan); threads without a candidate carry
+// (-inf, 0x7fffffff), so any real score beats them (scores can be negative
+// for user alpha/beta)
 template <int NT>
 __device__ __forceinline__ int block_argmax_double(double s, int idx, double* reds, int* redi) {
     constexpr int NW = NT / 32;
@@ -192,7 +188,7 @@ __device__ __forceinline__ int block_argmax_double(double s, int idx, double* re
     for (int o = 16; o > 0; o >>= 1) {
         const double s2 = __shfl_down_sync(FULLMASK, s, o);
         const int i2 = __shfl_down_sync(FULLMASK, idx, o);
-        if (argmax_better(s2, i2, s, idx)) {
+        if (s2 > s || (s2 == s && i2 < idx)) {
             s = s2;
             idx = i2;
         }
@@ -208,7 +204,7 @@ __device__ __forceinline__ int block_argmax_double(double s, int idx, double* re
     int bi = redi[0];
 #pragma unroll
     for (int w = 1; w < NW; ++w)
-        if (argmax_better(reds[w], redi[w], bs, bi)) {
+        if (reds[w] > bs || (reds[w] == bs && redi[w] < bi)) {
             bs = reds[w];
             bi = redi[w];
         }
@@ -423,7 +419,8 @@ struct St {
     }
     __device__ __forceinline__ int argmax(double s, int idx) {
         rsel ^= 1;
-        return block_argmax_double<NT>(s, idx, sp<double>(lay.reds) + rsel * NW, sp<int>(lay.redi) + rsel * NW);
+        const int q = block_argmax_double<NT>(s, idx, sp<double>(lay.reds) + rsel * NW, sp<int>(lay.redi) + rsel * NW);
+        return q == 0x7fffffff ? 0 : q;  // only for NaN scores: stay inside the list
     }
 
     // ---- mt19937_64, block-uniform: every thread walks the same stream
@@ -717,7 +714,8 @@ struct St {
         // the walk needs a non-decreasing running sum (beta >= 0, always true
         // for assign_strategies' slots); any other beta runs the reference loop
         const bool walk = !dense && beta >= 0.0;
-        __shared__ u32 s_wmax;  // max c - 1 over the list (walk: crossing bound)
+        // max c - 1 over the list (walk: crossing bound) in wbt's spare slot
+        u32* s_wmax = reinterpret_cast<u32*>(sp<double>(lay.wbt) + sd_ne + 1);
         const u32* ks = keys();
         const u16* c = cnts();
         const int V1 = V + 1;
@@ -734,7 +732,7 @@ struct St {
         for (int cc = tid; cc <= sd_ne; cc += NT)
             wbt[cc] = __dmul_rn(beta, double(cc - 1));
         if (tid == 0)
-            s_wmax = 0u;
+            *s_wmax = 0u;
         __syncthreads();
         // per-variable candidate counts (reference loop: total in nA; walk: A = as
         // second element, B = as first element)
@@ -758,7 +756,7 @@ struct St {
             }
             lmax = __reduce_max_sync(FULLMASK, lmax);
             if (lane == 0)
-                atomicMax(&s_wmax, lmax);
+                atomicMax(s_wmax, lmax);
         }
         __syncthreads();
         if (walk) {
@@ -822,9 +820,9 @@ struct St {
         }
         __syncthreads();
         last_coins = D;
-        double best_s = -1.0;
+        double best_s = -INFINITY;
         int best_q = 0x7fffffff;
-        const double topmin = double(s_wmax) + 1.0;
+        const double topmin = double(*s_wmax) + 1.0;
         if (walk) {
             u32* aoff = sp<u32>(lay.aoff);
             u32* cursor = sp<u32>(lay.cursor);
@@ -1010,7 +1008,7 @@ struct St {
     __device__ int sel_gp(double alpha) {
         const u32* ks = keys();
         const u16* c = cnts();
-        double best_s = -1.0;
+        double best_s = -INFINITY;
         int best_q = 0x7fffffff;
         for (int q = tid; q < m; q += NT) {
             const u32 kq = ks[q];
