@@ -179,7 +179,8 @@ typedef struct tcse_stats {
     uint64_t processes;    /* process runs */
     uint64_t launches;     /* search-kernel launches */
     int32_t iterations;    /* iteration barriers passed (max over systems) */
-    int32_t reserved;
+    int32_t retries;       /* iterations re-run at full candidate capacity (session layouts are
+                              sized from the starting list; results never depend on it) */
     double kernel_ms;      /* summed search-kernel time (CUDA events on the launch stream) */
     double step_ms;        /* summed iteration time on the device: search + reduce (CUDA events) */
     double wall_ms;        /* whole call, host clock */

@@ -85,7 +85,7 @@ class Stats(C.Structure):
         ("processes", C.c_uint64),
         ("launches", C.c_uint64),
         ("iterations", C.c_int32),
-        ("reserved", C.c_int32),
+        ("retries", C.c_int32),
         ("kernel_ms", C.c_double),
         ("step_ms", C.c_double),
         ("wall_ms", C.c_double),

@@ -261,6 +261,7 @@ struct DevSys {
     bool dense = true; // Greedy-Intersections form
     DBuf masks, keys, cnts;
     int base_m = 0;
+    int mcap_full = 0;  // > 0: h.mcap was shrunk to the starting list + slack
 };
 
 namespace {
@@ -311,6 +312,15 @@ void choose_launch(const tcse_ctx* ctx, DevSys* d) {
     if (!instantiated(d->W, nt))
         nt = 128;
     d->nt = nt;
+}
+
+// gi form on the actual starting list (lists only shrink): the dense
+// reference loop up to 512 candidates, the O(deg) walk beyond (sweep on every
+// fixture)
+void pick_form(DevSys* d) {
+    static const int dense_max = env_int("TCSE_GI_DENSE_MAX", 512);
+    if (env_int("TCSE_GI_DENSE", -1) < 0)
+        d->dense = d->base_m <= dense_max;
 }
 
 int smem_one(const DevSys& d) {
@@ -372,7 +382,7 @@ int check_err(tcse_ctx* ctx) {
     CU(cudaStreamSynchronize(ctx->stream));
     if (h[0] == TCSE_EREPLAY)
         return fail(TCSE_EREPLAY, "replay_prefix: unreplayable pair at position %d", h[1]);
-    if (h[0] == TCSE_ECAPACITY)
+    if (h[0] == TCSE_ECAPACITY || h[0] == kErrCandOverflow)
         return fail(TCSE_ECAPACITY, "device capacity exceeded (%d)", h[1]);
     if (h[0] != 0)
         return fail(h[0], "device error %d", h[0]);
@@ -449,13 +459,36 @@ int base_candidates(tcse_ctx* ctx, DevSys& d) {
     if (n > d.h.mcap)
         return fail(TCSE_ECAPACITY, "candidate capacity %d < %d", d.h.mcap, n);
     d.base_m = n;
-    // gi form on the actual starting list (lists only shrink): the dense
-    // reference loop up to 512 candidates, the O(deg) walk beyond (sweep on
-    // every fixture)
-    static const int dense_max = env_int("TCSE_GI_DENSE_MAX", 512);
-    if (env_int("TCSE_GI_DENSE", -1) < 0)
-        d.dense = n <= dense_max;
+    pick_form(&d);
     return TCSE_OK;
+}
+
+// Session layouts are sized for the starting list plus slack instead of the
+// worst-case bound (lists rarely grow: a substitution consumes its pair and
+// moves the others' occurrences to the fresh variable), e.g. 89 -> 64 KB per
+// process on 6x6x6 W (3 processes per SM instead of 2).  A process whose list
+// would outgrow the capacity flags kErrCandOverflow before writing; the
+// session then re-runs that iteration at full capacity (search_step_begin),
+// so results never depend on the slack.  TCSE_MCAP_SLACK=k: capacity m0 + k.
+void shrink_capacity(const tcse_ctx* ctx, DevSys* d) {
+    const int slack_env = env_int("TCSE_MCAP_SLACK", -1);
+    const int slack = slack_env >= 0 ? slack_env : d->base_m / 4 + 64;
+    const int eff = std::max(1, d->base_m + slack);
+    if (eff >= d->h.mcap)
+        return;
+    d->mcap_full = d->h.mcap;
+    d->h.mcap = eff;
+    choose_launch(ctx, d);
+    pick_form(d);
+}
+
+void restore_capacity(const tcse_ctx* ctx, DevSys* d) {
+    if (d->mcap_full == 0)
+        return;
+    d->h.mcap = d->mcap_full;
+    d->mcap_full = 0;
+    choose_launch(ctx, d);
+    pick_form(d);
 }
 
 int upload_pairs(tcse_ctx* ctx, const tcse_pair* pairs, int n, DBuf* buf) {
@@ -830,6 +863,8 @@ struct tcse_search {
     double kernel_ms = 0.0, step_ms = 0.0, exchange_ms = 0.0;
     int iteration = 0;
     bool stopped = false;
+    bool shrunk = false;  // some system runs with a shrunk candidate capacity
+    int retries = 0;      // iterations re-run at full capacity
     cudaEvent_t es0 = nullptr, es1 = nullptr;
     std::chrono::steady_clock::time_point t0;
     // exchange payload layout (int32 words): per system [n_max costs | 6 | sub_cap]
@@ -850,6 +885,35 @@ struct tcse_search {
 };
 
 namespace {
+
+// launch groups: systems with the same kernel instantiation share a launch;
+// groups after the first get their own stream
+int build_groups(tcse_search* S) {
+    tcse_ctx* ctx = S->ctx;
+    S->groups.clear();
+    for (int s = 0; s < S->n_systems; ++s) {
+        const DevSys& d = S->dev[size_t(s)];
+        bool placed = false;
+        for (auto& g : S->groups)
+            if (g.W == d.W && g.nt == d.nt && g.dense == d.dense) {
+                g.sys.push_back(s);
+                g.smem = std::max(g.smem, smem_one(d));
+                placed = true;
+            }
+        if (!placed)
+            S->groups.push_back({d.W, d.nt, d.dense, smem_one(d), {s}});
+    }
+    for (const auto& g : S->groups)
+        if (g.smem > 227 * 1024 - 1024)
+            return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", g.smem);
+    for (size_t g = 1; g < S->groups.size(); ++g) {
+        if (!ctx->aux[g - 1])
+            CU(cudaStreamCreateWithFlags(&ctx->aux[g - 1], cudaStreamNonBlocking));
+        if (!ctx->join[g - 1])
+            CU(cudaEventCreateWithFlags(&ctx->join[g - 1], cudaEventDisableTiming));
+    }
+    return TCSE_OK;
+}
 
 int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
                 const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb, void* user) {
@@ -885,26 +949,11 @@ int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_sys
         rc = base_candidates(ctx, d);
         if (rc)
             return rc;
-        // launch groups: systems with the same kernel instantiation share a launch
-        bool placed = false;
-        for (auto& g : S->groups)
-            if (g.W == d.W && g.nt == d.nt && g.dense == d.dense) {
-                g.sys.push_back(s);
-                g.smem = std::max(g.smem, smem_one(d));
-                placed = true;
-            }
-        if (!placed)
-            S->groups.push_back({d.W, d.nt, d.dense, smem_one(d), {s}});
+        shrink_capacity(ctx, &d);
+        S->shrunk = S->shrunk || d.mcap_full > 0;
     }
-    for (const auto& g : S->groups)
-        if (g.smem > 227 * 1024 - 1024)
-            return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", g.smem);
-    for (size_t g = 1; g < S->groups.size(); ++g) {
-        if (!ctx->aux[g - 1])
-            CU(cudaStreamCreateWithFlags(&ctx->aux[g - 1], cudaStreamNonBlocking));
-        if (!ctx->join[g - 1])
-            CU(cudaEventCreateWithFlags(&ctx->join[g - 1], cudaEventDisableTiming));
-    }
+    if ((rc = build_groups(S)))
+        return rc;
     if (!ctx->fork)
         CU(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
     for (int s = 0; s < n_systems; ++s) {
@@ -1000,6 +1049,7 @@ int search_step_begin(tcse_search* S, void* send_ext) {
         return rc;
     CU(cudaEventRecord(S->es0, ctx->stream));
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
+relaunch:
     CU(cudaEventRecord(ctx->fork, ctx->stream));
     int block_off = 0, n_aux = 0;
     for (size_t gi = 0; gi < S->groups.size(); ++gi) {
@@ -1062,6 +1112,24 @@ int search_step_begin(tcse_search* S, void* send_ext) {
     }
     for (int a = 0; a < n_aux; ++a)
         CU(cudaStreamWaitEvent(ctx->stream, ctx->join[a], 0));
+    if (S->shrunk) {
+        // a process outgrew a shrunk capacity: the same iteration again at
+        // full capacity (slots and streams are pure functions of the
+        // iteration, incumbent and reinit set, none of which changed)
+        int32_t h[2] = {0, 0};
+        CU(cudaMemcpyAsync(h, ctx->err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (h[0] == kErrCandOverflow) {
+            CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
+            for (int s = 0; s < S->n_systems; ++s)
+                restore_capacity(ctx, &S->dev[size_t(s)]);
+            S->shrunk = false;
+            ++S->retries;
+            if ((rc = build_groups(S)))
+                return rc;
+            goto relaunch;
+        }
+    }
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
     S->tx = std::chrono::steady_clock::now();
     int32_t* send = send_ext ? static_cast<int32_t*>(send_ext) : S->send.as<int32_t>();
@@ -1231,6 +1299,7 @@ int search_result(tcse_search* S, tcse_record* best, int32_t* iterations, tcse_s
         stats->processes = S->processes;
         stats->launches = S->launches;
         stats->iterations = S->iteration;
+        stats->retries = S->retries;
         stats->kernel_ms = S->kernel_ms;
         stats->step_ms = S->step_ms;
         stats->exchange_ms = S->exchange_ms;

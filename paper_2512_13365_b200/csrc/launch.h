@@ -30,6 +30,10 @@ enum Mode : int32_t {
     kModeDump = 2     // replay prefix, dump pairs (count_pairs parity hook / base candidates)
 };
 
+// device -> host only: a candidate list outgrew a shrunk session capacity
+// (the session re-runs the iteration at full capacity; never user-visible)
+constexpr int kErrCandOverflow = -100;
+
 struct SysDesc {
     // problem (base state, shared read-only by every block of the system)
     int32_t n_x, n_e, naive;

@@ -526,8 +526,9 @@ struct St {
         return c;
     }
 
-    // incremental candidate maintenance after q -> k (= V, 1-based)
-    __device__ void update(u32 q) {
+    // incremental candidate maintenance after q -> k (= V, 1-based); false if
+    // the new list would not fit the capacity (nothing written, block-uniform)
+    __device__ bool update(u32 q) {
         const int i = key_i(q), j = key_j(q);
         const int k = V;
         const u32* ok = keys();
@@ -580,6 +581,8 @@ struct St {
         u32 total;
         const u32 excl = block_scan<NT>(local, red(), &total);
         const u32 n_old = total & 0xffffu, n_new = total >> 16;
+        if (int(n_old + n_new) > mcap)
+            return false;
         u32 o = excl & 0xffffu, n = excl >> 16;
         for (int e = e0; e < e1; ++e) {
             if (e < m) {
@@ -633,6 +636,7 @@ struct St {
         __syncthreads();
         cur ^= 1;
         m = int(n_old + n_new);
+        return true;
     }
 
     // ---- selection strategies (strategies.hpp); return a candidate index
@@ -1074,6 +1078,7 @@ struct St {
     }
 
     int sd_ne;
+    int mcap;  // candidate capacity of the layout
 };
 
 // the system block `blk` belongs to (blocks are contiguous per system)
@@ -1163,6 +1168,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     pr.rsel = 0;
     pr.last_coins = 0;
     pr.sd_ne = sd.n_e;
+    pr.mcap = sd.mcap;
     if (sd.base_keys) {
         pr.m = sd.base_m;
     } else {
@@ -1246,7 +1252,10 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
                 sd.out_cost[lp] = -1;
             return;
         }
-        pr.update(q);
+        if (!pr.update(q)) {
+            set_error(sd, kErrCandOverflow, pr.m);
+            return;
+        }
         if (replay) {
             ++t_pre;
             if (!rec_prefix)
