@@ -73,6 +73,10 @@ def run(name, seed=1):
 
 if __name__ == "__main__":
     names = sys.argv[1:] or ["laderman", "sxs", "sxs_border", "naive555_f1000", "sxl", "naive666_f3000"]
+    # one untimed call first: CUDA context creation and module load are a
+    # one-time process cost, not part of any search (the reference arm runs
+    # in an already-loaded library too)
+    T.optimize_system((4, [[1, 2, -3, 4], [1, -2, -4], [1, -2, -3, 4]]), T.SearchConfig(n_processes=64, patience=1))
     rows = []
     for nm in names:
         r = run(nm)
