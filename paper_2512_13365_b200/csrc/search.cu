@@ -224,9 +224,64 @@ __device__ __noinline__ void mt_seed(u64* mt, u64 s) {
     }
 }
 
-// cooperative twist of the 312-word state (block-uniform call)
+// cooperative twist of the 312-word state (block-uniform call), two
+// barriers: thread i owns new[i] = mix(old[i], old[i+1], old[i+156]) and
+// new[156+i] = mix(old[156+i], old[157+i], new[i]); the one cross-thread
+// input, new[0] for new[311], is recomputed from old words by its owner.
+// COINS: also emit the generation's first n outputs as coin bits (tempered
+// top bit = parity of raw bits kCoinMask) at coin positions pos0 + e.
+template <int NT, bool COINS>
+__device__ __noinline__ void mt_twist_impl(u32* coin, u32 pos0, u32 n) {
+    constexpr int R = (156 + NT - 1) / NT;
+    u64* mt = sp<u64>(lay.mt);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    u64 lo[R], hi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < 156) {
+            const u64 o156 = mt[i + 156];
+            lo[r] = mt_mix(mt[i], mt[i + 1], o156);
+            const u64 nxt = i < 155 ? mt[i + 157] : mt_mix(mt[0], mt[1], mt[156]);  // old[312] := new[0]
+            hi[r] = mt_mix(o156, nxt, lo[r]);
+        }
+    }
+    if (COINS) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = tid + r * NT;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int e = i + half * 156;
+                const u32 bit = (i < 156 && u32(e) < n) ? (u32(__popcll((half ? hi[r] : lo[r]) & kCoinMask)) & 1u) : 0u;
+                const u32 ball = __ballot_sync(FULLMASK, bit);
+                if (lane == 0 && ball) {
+                    const u32 pos = pos0 + u32(e);
+                    const u32 w0 = pos >> 5, sh = pos & 31;
+                    atomicOr(&coin[w0], ball << sh);
+                    if (sh)
+                        atomicOr(&coin[w0 + 1], ball >> (32 - sh));
+                }
+            }
+        }
+    }
+    __syncthreads();  // every old word read
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < 156) {
+            mt[i] = lo[r];
+            mt[i + 156] = hi[r];
+        }
+    }
+    __syncthreads();  // new state visible
+}
+
+// small blocks (NT <= 64: R = 3..5 words per thread, one or two warps) keep
+// the register-light form: each phase read, barrier, write, barrier
 template <int NT>
-__device__ __noinline__ void mt_twist() {
+__device__ __noinline__ void mt_twist_small() {
     constexpr int R = (156 + NT - 1) / NT;
     u64* mt = sp<u64>(lay.mt);
     const int tid = threadIdx.x;
@@ -260,6 +315,14 @@ __device__ __noinline__ void mt_twist() {
             mt[i] = v[r];
     }
     __syncthreads();
+}
+
+template <int NT>
+__device__ __forceinline__ void mt_twist() {
+    if constexpr (NT >= 128)
+        mt_twist_impl<NT, false>(nullptr, 0u, 0u);
+    else
+        mt_twist_small<NT>();
 }
 
 struct Slot {
@@ -459,8 +522,17 @@ struct St {
         u32 done = 0;
         while (done < nbits) {
             if (mti >= 312) {
-                mt_twist<NT>();
-                mti = 0;
+                if constexpr (NT >= 128) {
+                    // fresh generation: twist and take its first n outputs in one pass
+                    const u32 n = min(312u, nbits - done);
+                    mt_twist_impl<NT, true>(coin, done, n);
+                    mti = int(n);
+                    done += n;
+                    continue;
+                } else {
+                    mt_twist<NT>();
+                    mti = 0;
+                }
             }
             const u32 n = min(u32(312 - mti), nbits - done);
             const u32 n32 = (n + 31) & ~31u;

@@ -1,5 +1,5 @@
 """Per-source-line hot spots from an ncu report (source page, cuda,sass view):
-python scripts/ncu_lines.py report.ncu-rep [top]"""
+python scripts/ncu_lines.py report.ncu-rep [top] [launch_skip launch_count]"""
 import csv
 import io
 import subprocess
@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+sel = ["--launch-skip", sys.argv[3], "--launch-count", sys.argv[4]] if len(sys.argv) > 4 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + sel,
                      capture_output=True, text=True).stdout
 rows = []
 fname = "?"
