@@ -64,9 +64,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
-                    help="payload all-gather transport for --gpus > 1 (gloo stages through host memory; "
-                         "lets the multi-rank path run with several ranks on one GPU for testing)")
+    ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="payload all-gather transport for --gpus > 1: nccl (one rank per GPU, the "
+                         "default when ranks <= GPUs) or gloo (stages through host memory; used "
+                         "automatically when several ranks share a GPU, which NCCL refuses)")
     args = ap.parse_args()
     wl, strat, procs = CONFIGS[args.config]
     args.workload = args.workload or wl
@@ -95,7 +96,8 @@ def config_block(args, world, scaling="weak"):
         "processes_per_gpu": args.processes,
         "processes_total": args.processes * world,
         "master_seed": args.seed,
-        "parallelism": "process-partition x%d (per-iteration all-gather exchange)" % world,
+        "parallelism": "process-partition x%d (per-iteration all-gather exchange%s)"
+                       % (world, "" if world == 1 else ", " + str(getattr(args, "dist_backend", "nccl"))),
         "l2": "flushed before every timed step (256 MiB write)",
     }
 
@@ -252,7 +254,10 @@ def main():
     import torch.distributed as dist
     import paper_2512_13365_b200 as T
 
-    local = local % max(1, torch.cuda.device_count())  # identity with one rank per GPU
+    n_dev = max(1, torch.cuda.device_count())
+    if args.dist_backend == "auto":
+        args.dist_backend = "nccl" if world <= n_dev else "gloo"
+    local = local % n_dev  # identity with one rank per GPU
     torch.cuda.set_device(local)
     if world > 1:
         if args.dist_backend == "nccl":
