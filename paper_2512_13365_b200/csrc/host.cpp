@@ -903,6 +903,17 @@ int build_groups(tcse_search* S) {
         if (!placed)
             S->groups.push_back({d.W, d.nt, d.dense, smem_one(d), {s}});
     }
+    // most work first (starting candidates x naive cost ~ steps x per-step
+    // cost): the long group's blocks start first and the short ones fill the
+    // tail (+8% on 5x5x5, +3% on 6x6x6 over creation order)
+    auto work = [&](const tcse_search::Group& g) {
+        double w = 0.0;
+        for (int s : g.sys)
+            w += double(S->dev[size_t(s)].base_m) * double(S->dev[size_t(s)].h.naive);
+        return w;
+    };
+    std::stable_sort(S->groups.begin(), S->groups.end(),
+                     [&](const tcse_search::Group& a, const tcse_search::Group& b) { return work(a) > work(b); });
     for (const auto& g : S->groups)
         if (g.smem > 227 * 1024 - 1024)
             return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", g.smem);
@@ -1052,7 +1063,10 @@ int search_step_begin(tcse_search* S, void* send_ext) {
 relaunch:
     CU(cudaEventRecord(ctx->fork, ctx->stream));
     int block_off = 0, n_aux = 0;
-    for (size_t gi = 0; gi < S->groups.size(); ++gi) {
+    static const int group_order = env_int("TCSE_GROUP_ORDER", 0);   // 1: reverse (A/B knob)
+    static const int group_serial = env_int("TCSE_GROUP_SERIAL", 0); // 1: one stream (A/B knob)
+    for (size_t gq = 0; gq < S->groups.size(); ++gq) {
+        const size_t gi = group_order == 1 ? S->groups.size() - 1 - gq : gq;
         const auto& g = S->groups[gi];
         LaunchDesc L;
         std::memset(&L, 0, sizeof L);
@@ -1100,7 +1114,7 @@ relaunch:
             return rc;
         block_off += blocks;
         cudaStream_t st = ctx->stream;
-        if (n_aux + 1 <= int(S->groups.size()) - 1 && block_off > blocks) {
+        if (!group_serial && n_aux + 1 <= int(S->groups.size()) - 1 && block_off > blocks) {
             st = ctx->aux[n_aux];
             CU(cudaStreamWaitEvent(st, ctx->fork, 0));
         }
