@@ -40,6 +40,9 @@ def run(name, seed=1):
     rj = json.loads(buf.value.decode())
     systems = [T.LinearSystem(nx, rows) for nx, rows in T.extract_systems(s)]
     N = gpu_count(s["r"])
+    # load this scheme's kernel shapes once (lazy module loading is a one-time
+    # process cost, not search time)
+    T.optimize_systems(systems, T.SearchConfig(n_processes=64, patience=1, max_iterations=1), [0, 1, 2])
     gcfg = T.SearchConfig(n_processes=N, master_seed=seed)
     start = time.time()
     stopped = {"flag": False}
@@ -58,6 +61,21 @@ def run(name, seed=1):
         ok, cost = T.verify_record(sys_, rec.substitutions)
         assert ok and cost == rec.cost
         costs.append(rec.cost)
+    # the rest of the budget: more seeds, then the reference's own component-
+    # wise combine (parallel_search.hpp:522-547) over every run
+    best = list(costs)
+    seeds = [seed]
+    nxt = seed + 1
+    while time.time() - start < t_ref:
+        scfg = T.SearchConfig(n_processes=N, master_seed=nxt)
+        r2 = T.optimize_systems(systems, scfg, [0, 1, 2], on_iteration=on_it)
+        for c, (sys_, (rec, _)) in enumerate(zip(systems, r2)):
+            ok, cost = T.verify_record(sys_, rec.substitutions)
+            assert ok and cost == rec.cost
+            best[c] = min(best[c], rec.cost)
+        seeds.append(nxt)
+        nxt += 1
+    t_all = time.time() - start
     return {
         "scheme": name, "digest": T.scheme_digest(s), "shape": "%dx%dx%d:%d" % (s["m"], s["n"], s["p"], s["r"]),
         "naive": [T.naive_cost(r) for _, r in T.extract_systems(s)],
@@ -68,6 +86,9 @@ def run(name, seed=1):
                 "wall_s": round(t_gpu, 3), "stopped_at_budget": stopped["flag"], "steps": st["steps"],
                 "steps_per_s_device": st["steps"] / max(1e-9, st["kernel_ms"]) * 1e3},
         "gpu_le_reference": sum(costs) <= rj["total"],
+        "gpu_seeds_combined": {"total": sum(best), "components": best, "seeds": seeds, "wall_s": round(t_all, 3),
+                               "note": "runs with master seeds %d..%d until the reference's wall time, "
+                                       "component-wise minimum (the reference's combine)" % (seeds[0], seeds[-1])},
     }
 
 
