@@ -392,6 +392,10 @@ def main():
             pct = lambda k: float(str(nj.get(k, "nan")).split()[0])  # noqa: E731
             issue = {"issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                      "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                     "alu_pipe_pct": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                     "lsu_pipe_pct": pct("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                     "smem_wavefronts_pct": pct(
+                         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
                      "source": "profiles/" + name}
             break
     line = {
