@@ -398,6 +398,7 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.words = d.h.w_need;
     sd.coin_words = coin_words_for(d.h);
     sd.gi_dense = d.dense ? 1 : 0;
+    sd.gi_prune = env_int("TCSE_GI_PRUNE", 1);
     sd.vcap = d.h.vcap;
     sd.mcap = d.h.mcap;
     sd.sub_cap = d.h.naive / 2 + 1;

@@ -61,6 +61,9 @@ constexpr u64 kMtLM = 0x7fffffffULL;
 constexpr u64 kMtA = 0xb5026f5aa96619e9ULL;
 constexpr u64 kMtF = 6364136223846793005ULL;
 // top bit of the tempered output = parity of these raw state bits
+#ifndef TCSE_FUSED_TWIST_MIN
+#define TCSE_FUSED_TWIST_MIN 128  // block sizes that twist in one fused two-barrier pass
+#endif
 constexpr u64 kCoinMask = 0x8080000004000200ULL;
 
 __device__ __forceinline__ u64 mt_temper(u64 z) {
@@ -319,7 +322,7 @@ __device__ __noinline__ void mt_twist_small() {
 
 template <int NT>
 __device__ __forceinline__ void mt_twist() {
-    if constexpr (NT >= 128)
+    if constexpr (NT >= TCSE_FUSED_TWIST_MIN)
         mt_twist_impl<NT, false>(nullptr, 0u, 0u);
     else
         mt_twist_small<NT>();
@@ -522,7 +525,7 @@ struct St {
         u32 done = 0;
         while (done < nbits) {
             if (mti >= 312) {
-                if constexpr (NT >= 128) {
+                if constexpr (NT >= TCSE_FUSED_TWIST_MIN) {
                     // fresh generation: twist and take its first n outputs in one pass
                     const u32 n = min(312u, nbits - done);
                     mt_twist_impl<NT, true>(coin, done, n);
@@ -800,6 +803,7 @@ struct St {
         u32* qbase = sp<u32>(lay.qbase);
         double* wbt = sp<double>(lay.wbt);
         const u32* coin = sp<u32>(lay.coin);
+        // @region gi_zero
         for (int v = tid; v < V1; v += NT) {
             nA[v] = 0u;
             if (walk)
@@ -810,6 +814,7 @@ struct St {
         if (tid == 0)
             *s_wmax = 0u;
         __syncthreads();
+        // @region gi_counts
         // per-variable candidate counts (reference loop: total in nA; walk: A = as
         // second element, B = as first element)
         if (!walk) {
@@ -836,6 +841,7 @@ struct St {
         }
         __syncthreads();
         if (walk) {
+            // @region gi_aoff
             // A-list offsets: scan over variables
             u32* aoff = sp<u32>(lay.aoff);
             u32* cursor = sp<u32>(lay.cursor);
@@ -852,6 +858,7 @@ struct St {
                 ex += nA[e];
             }
         }
+        // @region gi_deg_scan
         // coins per q = candidates sharing a variable, minus q itself (and its
         // opposite-sign twin, counted under both variables); w prefix sums
         const int E = (m + NT - 1) / NT;
@@ -905,6 +912,7 @@ struct St {
             u32* bs = sp<u32>(lay.bs);
             u16* alist = sp<u16>(lay.alist);
             const u32* wp = sp<u32>(lay.wp);
+            // @region gi_alist
             // A lists: candidate indices by second element, index order
             for (int t = tid; t < m; t += NT)
                 alist[atomicAdd(&cursor[key_j(ks[t])], 1u)] = u16(t);
@@ -922,8 +930,22 @@ struct St {
                     alist[b0 + y + 1] = t;
                 }
             }
-            // coins in chunks of candidates whose coins fit the buffer
+            // Scores in chunks of candidates whose coins fit the buffer.
+            // prune: every candidate first gets an approximate score from
+            // exact integer sums (disjoint weight D_q, coin-weighted
+            // intersecting weight C_q): H~ = w_q + a (D_q + b C_q).  The
+            // reference's sequential double H differs from H~ by at most
+            // eps (recursive-summation bound, 4x margin: DESIGN.md section 3),
+            // so only candidates with H~ >= max H~ - 2 eps can be the
+            // reference's pick; those alone are folded exactly (the walk
+            // below, bit-identical to score_intersections_from) while their
+            // coins are still in the buffer, and the exact scores decide.
             const u32 cap = lay.coin_cap;
+            const u32 T = wp[m];
+            const double eps =
+                ldexp(double(m + 16) * (double(*s_wmax) + fabs(alpha) * double(T) * fmax(1.0, beta)), -51);
+            const double eps2 = __dmul_rn(2.0, eps);
+            double B = -INFINITY;  // running max of the approximate scores
             int q_lo = 0;
             while (q_lo < m) {
                 const u32 c0 = qbase[q_lo];
@@ -936,41 +958,58 @@ struct St {
                         hi = mid - 1;
                 }
                 const int q_hi = lo;
+                // @region gi_coins
                 draw_coins(qbase[q_hi] - c0);  // barrier-separated clear, ends with a barrier
-                for (int q = q_lo + tid; q < q_hi; q += NT) {
-                    const u32 kq = ks[q];
-                    const int qi = key_i(kq), qj = key_j(kq);
-                    const int ai = int(aoff[qi]), nai = int(nA[qi]), bi = int(bs[qi]), li = nai + int(nB[qi]);
-                    const int aj = int(aoff[qj]), naj = int(nA[qj]), bj = int(bs[qj]), lj = naj + int(nB[qj]);
-                    u32 ptr = qbase[q] - c0;
-                    double f = 0.0;
-                    int prev = 0, pi = 0, pj = 0;
-                    for (;;) {
-                        const int xi = pi < li ? (pi < nai ? int(alist[ai + pi]) : bi + (pi - nai)) : 0x7fffffff;
-                        const int xj = pj < lj ? (pj < naj ? int(alist[aj + pj]) : bj + (pj - naj)) : 0x7fffffff;
-                        const int s = min(xi, xj);
-                        pi += xi == s;
-                        pj += xj == s;
-                        f = add_run(f, prev, s == 0x7fffffff ? m : s, wp, topmin);
-                        if (s == 0x7fffffff)
-                            break;
-                        prev = s + 1;
-                        if (s != q) {
-                            if ((coin[ptr >> 5] >> (ptr & 31u)) & 1u)
-                                f = __dadd_rn(f, wbt[c[s]]);
-                            ++ptr;
+                // @region gi_approx_pass
+                if (!gi_prune) {
+                    for (int q = q_lo + tid; q < q_hi; q += NT) {
+                        const double h = gi_fold(q, c0, alpha, topmin);
+                        if (h > best_s || best_q == 0x7fffffff) {
+                            best_s = h;
+                            best_q = q;
                         }
                     }
-                    const double h = __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, f));
-                    if (h > best_s || best_q == 0x7fffffff) {
-                        best_s = h;
-                        best_q = q;
+                } else {
+                    double lb = -INFINITY, h1 = 0.0, h2 = 0.0;
+                    int q1 = -1, q2 = -1;
+                    bool ovf = false;
+                    for (int q = q_lo + tid; q < q_hi; q += NT) {
+                        const double h = gi_approx(q, c0, T, alpha, beta);
+                        lb = fmax(lb, h);
+                        const double lim = __dsub_rn(lb, eps2);
+                        if (q1 >= 0 && h1 < lim)
+                            q1 = -1;
+                        if (q2 >= 0 && h2 < lim)
+                            q2 = -1;
+                        if (h >= lim) {
+                            if (q1 < 0) {
+                                q1 = q;
+                                h1 = h;
+                            } else if (q2 < 0) {
+                                q2 = q;
+                                h2 = h;
+                            } else {
+                                ovf = true;
+                            }
+                        }
+                    }
+                    // @region gi_folds
+                    B = fmax(B, block_max_d(lb));
+                    const double thr = __dsub_rn(B, eps2);
+                    if (ovf) {  // more than two near-ties in one thread: rescan
+                        gi_rescan(q_lo, q_hi, c0, T, alpha, beta, topmin, thr, best_s, best_q);
+                    } else {
+                        if (q1 >= 0 && h1 >= thr)
+                            gi_keep(gi_fold(q1, c0, alpha, topmin), q1, best_s, best_q);
+                        if (q2 >= 0 && h2 >= thr)
+                            gi_keep(gi_fold(q2, c0, alpha, topmin), q2, best_s, best_q);
                     }
                 }
                 __syncthreads();
                 q_lo = q_hi;
             }
         } else {
+            // @region gi_dense_loop
             // the reference loop itself, coins in chunks; each thread carries
             // up to K candidates through one pass (K independent double chains)
             constexpr int K = 3;
@@ -1034,7 +1073,117 @@ struct St {
                 q_lo = q_hi;
             }
         }
+        // @region gi_argmax
         return argmax(best_s, best_q);
+    }
+
+    __device__ __forceinline__ static void gi_keep(double h, int q, double& best_s, int& best_q) {
+        if (h > best_s || (h == best_s && q < best_q) || best_q == 0x7fffffff) {
+            best_s = h;
+            best_q = q;
+        }
+    }
+
+    __device__ __forceinline__ double block_max_d(double v) {
+        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 16));
+        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 8));
+        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 4));
+        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 2));
+        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 1));
+        if (NW == 1)
+            return v;
+        rsel ^= 1;
+        double* r = sp<double>(lay.reds) + rsel * NW;
+        if (lane == 0)
+            r[tid >> 5] = v;
+        __syncthreads();
+        double b = r[0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w)
+            b = fmax(b, r[w]);
+        return b;
+    }
+
+    // Candidate q's intersecting candidates in canonical order: the merge of
+    // variable qi's and qj's lists (A list = candidates holding the variable
+    // second, by index; then the contiguous run holding it first).  q itself
+    // and its opposite-sign twin appear in both and are visited once.
+    template <typename F>
+    __device__ __forceinline__ void gi_neighbours(int q, F&& visit) {
+        const u32 kq = keys()[q];
+        const int qi = key_i(kq), qj = key_j(kq);
+        const u32* aoff = sp<u32>(lay.aoff);
+        const u32* nA = sp<u32>(lay.nA);
+        const u32* nB = sp<u32>(lay.nB);
+        const u32* bs = sp<u32>(lay.bs);
+        const u16* alist = sp<u16>(lay.alist);
+        const int ai = int(aoff[qi]), nai = int(nA[qi]), bi = int(bs[qi]), li = nai + int(nB[qi]);
+        const int aj = int(aoff[qj]), naj = int(nA[qj]), bj = int(bs[qj]), lj = naj + int(nB[qj]);
+        int pi = 0, pj = 0;
+        for (;;) {
+            const int xi = pi < li ? (pi < nai ? int(alist[ai + pi]) : bi + (pi - nai)) : 0x7fffffff;
+            const int xj = pj < lj ? (pj < naj ? int(alist[aj + pj]) : bj + (pj - naj)) : 0x7fffffff;
+            const int s = min(xi, xj);
+            pi += xi == s;
+            pj += xj == s;
+            if (!visit(s))
+                break;
+        }
+    }
+
+    // approximate gi score of q: exact integer sums, three roundings
+    __device__ __forceinline__ double gi_approx(int q, u32 c0, u32 T, double alpha, double beta) {
+        const u16* c = cnts();
+        const u32* coin = sp<u32>(lay.coin);
+        u32 ptr = sp<u32>(lay.qbase)[q] - c0;
+        u32 I = 0, C = 0;
+        gi_neighbours(q, [&](int s) {
+            if (s == 0x7fffffff)
+                return false;
+            if (s != q) {
+                const u32 w = u32(c[s]) - 1u;
+                I += w;
+                C += ((coin[ptr >> 5] >> (ptr & 31u)) & 1u) ? w : 0u;
+                ++ptr;
+            }
+            return true;
+        });
+        const u32 wq = u32(c[q]) - 1u;
+        const double F = __dadd_rn(double(T - wq - I), __dmul_rn(beta, double(C)));
+        return __dadd_rn(double(wq), __dmul_rn(alpha, F));
+    }
+
+    __device__ __noinline__ void gi_rescan(int q_lo, int q_hi, u32 c0, u32 T, double alpha, double beta,
+                                           double topmin, double thr, double& best_s, int& best_q) {
+        for (int q = q_lo + tid; q < q_hi; q += NT)
+            if (gi_approx(q, c0, T, alpha, beta) >= thr)
+                gi_keep(gi_fold(q, c0, alpha, topmin), q, best_s, best_q);
+    }
+
+    // exact gi score of q: score_intersections_from's sequential sum, runs of
+    // disjoint candidates added in O(1) by add_run
+    __device__ __noinline__ double gi_fold(int q, u32 c0, double alpha, double topmin) {
+        const u16* c = cnts();
+        const u32* coin = sp<u32>(lay.coin);
+        const u32* wp = sp<u32>(lay.wp);
+        const double* wbt = sp<double>(lay.wbt);
+        const int m_ = m;
+        u32 ptr = sp<u32>(lay.qbase)[q] - c0;
+        double f = 0.0;
+        int prev = 0;
+        gi_neighbours(q, [&](int s) {
+            f = add_run(f, prev, s == 0x7fffffff ? m_ : s, wp, topmin);
+            if (s == 0x7fffffff)
+                return false;
+            prev = s + 1;
+            if (s != q) {
+                if ((coin[ptr >> 5] >> (ptr & 31u)) & 1u)
+                    f = __dadd_rn(f, wbt[c[s]]);
+                ++ptr;
+            }
+            return true;
+        });
+        return __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, f));
     }
 
     // Sequential double sum f + w_L + ... + w_{R-1} (w_t = c_t - 1 >= 1,
@@ -1150,6 +1299,7 @@ struct St {
     }
 
     int sd_ne;
+    int gi_prune;  // 0: fold every candidate exactly (test hook)
     int mcap;  // candidate capacity of the layout
 };
 
@@ -1240,6 +1390,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     pr.rsel = 0;
     pr.last_coins = 0;
     pr.sd_ne = sd.n_e;
+    pr.gi_prune = sd.gi_prune;
     pr.mcap = sd.mcap;
     if (sd.base_keys) {
         pr.m = sd.base_m;

@@ -1,6 +1,9 @@
 """Both exact Greedy-Intersections forms against the oracle (search.cu
 sel_gi / add_run): the dense reference loop (TCSE_GI_DENSE=1) and the O(deg)
-walk (TCSE_GI_DENSE=0), forced on the same processes.
+walk (TCSE_GI_DENSE=0), forced on the same processes — the walk both with
+near-best pruning (default: approximate scores from exact integer sums, exact
+folds only within the rounding bound of the best) and folding every candidate
+(TCSE_GI_PRUNE=0).
 
 The walk adds runs of disjoint candidates in O(1), including the binade
 crossings of the running double sum: by binary search below max(c-1)+1 and
@@ -41,16 +44,31 @@ def gi_cfgs(rng, n):
     return out
 
 
+def cyclic_system(n, offsets, copies):
+    """Rows {r, r+o1, r+o2, ...} (mod n), each repeated: every candidate has the
+    same count and the same number of intersecting candidates, so approximate
+    gi scores tie exactly whenever coin sums do (the pruned walk then folds
+    several near-best candidates per thread, including its rescan path)."""
+    rows = []
+    for r in range(n):
+        row = [(r + o) % n + 1 for o in offsets]
+        for k in range(copies):
+            rows.append([v if (k + i) % 3 else -v for i, v in enumerate(row)] if k % 2 else list(row))
+    return n, rows
+
+
 def systems(rng):
     out = [random_system(rng, 40, 12) for _ in range(4)]
+    out += [cyclic_system(100, (0, 1, 3), 2), cyclic_system(64, (0, 1, 2, 5), 3)]
     out += [tall_system(rng, 90, 8, 0.45), tall_system(rng, 200, 9, 0.35), tall_system(rng, 250, 14, 0.2)]
     out += [fixture_systems("sxs")[2], fixture_systems("naive555_f1000")[2]]
     return out
 
 
-@pytest.mark.parametrize("form", ["1", "0"])
+@pytest.mark.parametrize("form", ["1", "0", "0-exact"])
 def test_gi_forms_match_oracle(dev, monkeypatch, form):
-    monkeypatch.setenv("TCSE_GI_DENSE", form)
+    monkeypatch.setenv("TCSE_GI_DENSE", form[0])
+    monkeypatch.setenv("TCSE_GI_PRUNE", "0" if form.endswith("exact") else "1")
     rng = random.Random(4242)
     for sys_ in systems(rng):
         cfgs = gi_cfgs(rng, 18)
