@@ -225,8 +225,10 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
         o += al16((vc + 1u) * 4u);
         L->alist = o;
         o += al16(mc * 2u);
-    } else {
-        L->wp = L->nB = L->aoff = L->bs = L->cursor = L->alist = L->nA;
+    } else {  // dense view: prefix sums for the exact folds of near-best candidates
+        L->wp = o;
+        o += al16((mc + 1u) * 4u);
+        L->nB = L->aoff = L->bs = L->cursor = L->alist = L->nA;
     }
     L->wbt = o;
     o += al16(u32(n_e + 2) * 8u);

@@ -102,6 +102,9 @@ __device__ __forceinline__ double uniform_real(u64 x, double a, double b) {
 
 __shared__ Lay lay;
 
+__device__ __forceinline__ double __int_as_double_lo(int v) { return __hiloint2double(0, v); }
+__device__ __forceinline__ int __double_lo_as_int(double d) { return __double2loint(d); }
+
 template <typename T>
 __device__ __forceinline__ T* sp(u32 off) {
     return reinterpret_cast<T*>(g_smem + off);
@@ -148,6 +151,15 @@ __device__ __forceinline__ u32 block_scan(u32 v, u32* red, u32* total) {
     return red[warp] + inc - v;
 }
 
+// out of line (one copy per kernel instead of one per call site): low 32
+// bits the exclusive prefix, high 32 bits the block total
+template <int NT>
+__device__ __noinline__ u64 block_scan_ool(u32 v, u32* red) {
+    u32 total;
+    const u32 ex = block_scan<NT>(v, red, &total);
+    return (u64(total) << 32) | ex;
+}
+
 template <int NT>
 __device__ __forceinline__ u32 block_max(u32 v, u32* red) {
     constexpr int NW = NT / 32;
@@ -185,7 +197,7 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* red) {
 // (-inf, 0x7fffffff), so any real score beats them (scores can be negative
 // for user alpha/beta)
 template <int NT>
-__device__ __forceinline__ int block_argmax_double(double s, int idx, double* reds, int* redi) {
+__device__ __noinline__ int block_argmax_double(double s, int idx, double* reds, int* redi) {
     constexpr int NW = NT / 32;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -519,6 +531,7 @@ struct St {
     __device__ void draw_coins(u32 nbits) {
         u32* coin = sp<u32>(lay.coin);
         const u32 words = (nbits + 31) >> 5;
+#pragma unroll 1
         for (u32 w = tid; w < words; w += NT)
             coin[w] = 0u;
         __syncthreads();
@@ -614,6 +627,7 @@ struct St {
         u32* aux = sp<u32>(lay.aux);
         u32* newexcl = sp<u32>(lay.newexcl);
         // (a) recount old candidates touching i or j (their counts only drop)
+#pragma unroll 1
         for (int t = tid; t < m; t += NT) {
             const u32 kk = ok[t];
             const int a = key_i(kk), b = key_j(kk);
@@ -627,6 +641,7 @@ struct St {
             kp[w] = pk[w];
             kn[w] = pk[W + w];
         }
+#pragma unroll 1
         for (int x = tid + 1; x < k; x += NT) {
             const u64* px = P(x - 1);
             int cp = 0, cn = 0;
@@ -644,6 +659,7 @@ struct St {
         const int E = (L + NT - 1) / NT;
         const int e0 = min(L, tid * E), e1 = min(L, e0 + E);
         u32 local = 0;
+#pragma unroll 1
         for (int e = e0; e < e1; ++e) {
             if (e < m) {
                 local += tcnt[e] >= 2 ? 1u : 0u;
@@ -654,11 +670,14 @@ struct St {
             }
         }
         u32 total;
-        const u32 excl = block_scan<NT>(local, red(), &total);
+        const u64 sc_excl = block_scan_ool<NT>(local, red());
+        u32 excl = u32(sc_excl);
+        total = u32(sc_excl >> 32);
         const u32 n_old = total & 0xffffu, n_new = total >> 16;
         if (int(n_old + n_new) > mcap)
             return false;
         u32 o = excl & 0xffffu, n = excl >> 16;
+#pragma unroll 1
         for (int e = e0; e < e1; ++e) {
             if (e < m) {
                 aux[e] = o;
@@ -676,6 +695,7 @@ struct St {
         u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
         o = excl & 0xffffu;
         n = excl >> 16;
+#pragma unroll 1
         for (int e = e0; e < e1; ++e) {
             if (e < m) {
                 if (tcnt[e] >= 2) {
@@ -720,6 +740,7 @@ struct St {
     __device__ int sel_greedy() {
         const u16* c = cnts();
         u32 best = 0;
+#pragma unroll 1
         for (int t = tid; t < m; t += NT)
             best = max(best, (u32(c[t]) << 16) | (0xffffu - u32(t)));
         best = block_max<NT>(best, red());
@@ -730,10 +751,12 @@ struct St {
     __device__ int sel_ga() {
         const u16* c = cnts();
         u32 mx = 0;
+#pragma unroll 1
         for (int t = tid; t < m; t += NT)
             mx = max(mx, u32(c[t]));
         mx = block_max<NT>(mx, red());
         u32 cnt = 0;
+#pragma unroll 1
         for (int t = tid; t < m; t += NT)
             cnt += c[t] == mx ? 1u : 0u;
         cnt = block_sum<NT>(cnt, red());
@@ -741,11 +764,15 @@ struct St {
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
         u32 local = 0;
+#pragma unroll 1
         for (int e = e0; e < e1; ++e)
             local += c[e] == mx ? 1u : 0u;
         u32 total;
-        u32 ex = block_scan<NT>(local, red(), &total);
+        const u64 sc_ex = block_scan_ool<NT>(local, red());
+        u32 ex = u32(sc_ex);
+        total = u32(sc_ex >> 32);
         u32* bc = sp<u32>(lay.bcast);
+#pragma unroll 1
         for (int e = e0; e < e1; ++e)
             if (c[e] == mx) {
                 if (ex == r)
@@ -761,6 +788,7 @@ struct St {
         const u16* c = cnts();
         u32* bc = sp<u32>(lay.bcast);
         u32 tot = 0;
+#pragma unroll 1
         for (int t = tid; t < m; t += NT)
             tot += u32(c[t]) - 1u;
         tot = block_sum<NT>(tot, red());
@@ -771,10 +799,14 @@ struct St {
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
         u32 local = 0;
+#pragma unroll 1
         for (int e = e0; e < e1; ++e)
             local += u32(c[e]) - 1u;
         u32 total;
-        u32 s = block_scan<NT>(local, red(), &total);
+        const u64 sc_s = block_scan_ool<NT>(local, red());
+        u32 s = u32(sc_s);
+        total = u32(sc_s >> 32);
+#pragma unroll 1
         for (int e = e0; e < e1; ++e) {
             const u32 s1 = s + u32(c[e]) - 1u;
             if (double(s1) > target && double(s) <= target)
@@ -793,8 +825,13 @@ struct St {
         // the walk needs a non-decreasing running sum (beta >= 0, always true
         // for assign_strategies' slots); any other beta runs the reference loop
         const bool walk = !dense && beta >= 0.0;
-        // max c - 1 over the list (walk: crossing bound) in wbt's spare slot
+        // dense form with near-best pruning: integer score sums in the
+        // candidate loop, exact folds only for near-ties (same bound as the walk)
+        const bool approx = dense && gi_prune && beta >= 0.0;
+        // max c - 1 over the list (crossing bound) and max coins per candidate
+        // in wbt's spare slot
         u32* s_wmax = reinterpret_cast<u32*>(sp<double>(lay.wbt) + sd_ne + 1);
+        u32* s_dmax = s_wmax + 1;
         const u32* ks = keys();
         const u16* c = cnts();
         const int V1 = V + 1;
@@ -804,28 +841,41 @@ struct St {
         double* wbt = sp<double>(lay.wbt);
         const u32* coin = sp<u32>(lay.coin);
         // @region gi_zero
+#pragma unroll 1
         for (int v = tid; v < V1; v += NT) {
             nA[v] = 0u;
             if (walk)
                 nB[v] = 0u;
         }
+#pragma unroll 1
         for (int cc = tid; cc <= sd_ne; cc += NT)
             wbt[cc] = __dmul_rn(beta, double(cc - 1));
-        if (tid == 0)
+        if (tid == 0) {
             *s_wmax = 0u;
+            *s_dmax = 0u;
+        }
         __syncthreads();
         // @region gi_counts
         // per-variable candidate counts (reference loop: total in nA; walk: A = as
         // second element, B = as first element)
         if (!walk) {
+            u32 lmax = 0u;
+#pragma unroll 1
             for (int t = tid; t < m; t += NT) {
                 const u32 kk = ks[t];
                 atomicAdd(&nA[key_i(kk)], 1u);
                 atomicAdd(&nA[key_j(kk)], 1u);
+                lmax = max(lmax, u32(c[t]) - 1u);
+            }
+            if (approx) {
+                lmax = __reduce_max_sync(FULLMASK, lmax);
+                if (lane == 0)
+                    atomicMax(s_wmax, lmax);
             }
         } else {
             u32* bs = sp<u32>(lay.bs);
             u32 lmax = 0u;
+#pragma unroll 1
             for (int t = tid; t < m; t += NT) {
                 const u32 kk = ks[t];
                 const int a = key_i(kk), b = key_j(kk);
@@ -848,10 +898,14 @@ struct St {
             const int E = (V1 + NT - 1) / NT;
             const int e0 = min(V1, tid * E), e1 = min(V1, e0 + E);
             u32 local = 0;
+#pragma unroll 1
             for (int e = e0; e < e1; ++e)
                 local += nA[e];
             u32 total;
-            u32 ex = block_scan<NT>(local, red(), &total);
+            const u64 sc_ex = block_scan_ool<NT>(local, red());
+            u32 ex = u32(sc_ex);
+            total = u32(sc_ex >> 32);
+#pragma unroll 1
             for (int e = e0; e < e1; ++e) {
                 aoff[e] = ex;
                 cursor[e] = ex;
@@ -865,7 +919,8 @@ struct St {
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
         u32 D;
         {
-            u32 ld = 0, lw = 0;
+            u32 ld = 0, lw = 0, dmax = 0;
+#pragma unroll 1
             for (int e = e0; e < e1; ++e) {
                 const u32 kk = ks[e];
                 const u32 twin = (e + 1 < m && ks[e + 1] == (kk | 1u) && !(kk & 1u)) ||
@@ -873,31 +928,40 @@ struct St {
                                      ? 1u
                                      : 0u;
                 const int a = key_i(kk), b = key_j(kk);
-                ld += !walk ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
+                const u32 dq = !walk ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
+                qbase[e] = dq;  // this thread's range only; prefix below
+                ld += dq;
+                dmax = max(dmax, dq);
                 lw += u32(c[e]) - 1u;
             }
-            u32 exd = block_scan<NT>(ld, red(), &D);
+            if (approx) {
+                dmax = __reduce_max_sync(FULLMASK, dmax);
+                if (lane == 0)
+                    atomicMax(s_dmax, dmax);
+            }
+            const u64 sc_exd = block_scan_ool<NT>(ld, red());
+            u32 exd = u32(sc_exd);
+            D = u32(sc_exd >> 32);
             u32 W_ = 0, exw = 0;
-            if (walk)
-                exw = block_scan<NT>(lw, red(), &W_);
+            if (walk || approx) {
+                const u64 sc_w = block_scan_ool<NT>(lw, red());
+                exw = u32(sc_w);
+                W_ = u32(sc_w >> 32);
+            }
             u32* wp = sp<u32>(lay.wp);
+#pragma unroll 1
             for (int e = e0; e < e1; ++e) {
-                const u32 kk = ks[e];
-                const u32 twin = (e + 1 < m && ks[e + 1] == (kk | 1u) && !(kk & 1u)) ||
-                                         (e > 0 && (kk & 1u) && ks[e - 1] == (kk & ~1u))
-                                     ? 1u
-                                     : 0u;
-                const int a = key_i(kk), b = key_j(kk);
+                const u32 dq = qbase[e];
                 qbase[e] = exd;
-                exd += !walk ? nA[a] + nA[b] - 2u - twin : nA[a] + nB[a] + nA[b] + nB[b] - 2u - twin;
-                if (walk) {
+                exd += dq;
+                if (walk || approx) {
                     wp[e] = exw;
                     exw += u32(c[e]) - 1u;
                 }
             }
             if (tid == 0) {
                 qbase[m] = D;
-                if (walk)
+                if (walk || approx)
                     wp[m] = W_;
             }
         }
@@ -914,9 +978,11 @@ struct St {
             const u32* wp = sp<u32>(lay.wp);
             // @region gi_alist
             // A lists: candidate indices by second element, index order
+#pragma unroll 1
             for (int t = tid; t < m; t += NT)
                 alist[atomicAdd(&cursor[key_j(ks[t])], 1u)] = u16(t);
             __syncthreads();
+#pragma unroll 1
             for (int v = tid; v < V1; v += NT) {
                 const int b0 = int(aoff[v]), n = int(nA[v]);
 #pragma unroll 1
@@ -1009,11 +1075,27 @@ struct St {
                 q_lo = q_hi;
             }
         } else {
-            // @region gi_dense_loop
-            // the reference loop itself, coins in chunks; each thread carries
-            // up to K candidates through one pass (K independent double chains)
-            constexpr int K = 3;
+            // @region gi_dense
+            // Dense layout.  With near-best pruning (approx; needs T < 2^16 and
+            // at most 64 coins per candidate) one pass per coin chunk computes
+            // every candidate's exact integer sums (intersecting weight I_q and
+            // its coin-selected part C_q, packed I << 16 | C) and the
+            // approximate score w_q + a (T - w_q - I_q + b C_q) — within eps of
+            // the reference's sequential double (the walk's bound).  Only
+            // candidates within 2 eps of the best approximate score can be the
+            // reference's pick: a lone one is the pick; several are folded
+            // exactly (gi_fold_dense, one warp per candidate) and the exact
+            // scores decide.  A thread with more than two near-best candidates,
+            // or the layout without pruning, runs the reference loop itself
+            // (gi_dense_chunk).
             const u32 cap = lay.coin_cap;
+            const bool use_approx = approx && wp_total() < 65536u && *s_dmax <= 64u;
+            const u32 T = use_approx ? wp_total() : 0u;
+            const double eps = use_approx ? ldexp(double(m + 16) * (double(*s_wmax) +
+                                                                    fabs(alpha) * double(T) * fmax(1.0, beta)), -51)
+                                          : 0.0;
+            const double eps2 = __dmul_rn(2.0, eps);
+            double B = -INFINITY;
             int q_lo = 0;
             while (q_lo < m) {
                 const u32 c0 = qbase[q_lo];
@@ -1027,47 +1109,54 @@ struct St {
                 }
                 const int q_hi = lo;
                 draw_coins(qbase[q_hi] - c0);
-                for (int q0 = q_lo + tid; q0 < q_hi; q0 += K * NT) {
-                    int qv[K], qi[K], qj[K];
-                    u32 ptr[K];
-                    double fut[K];
-#pragma unroll
-                    for (int t = 0; t < K; ++t) {
-                        qv[t] = q0 + t * NT;
-                        const bool on = qv[t] < q_hi;
-                        const u32 kq = on ? ks[qv[t]] : 0u;
-                        qi[t] = on ? key_i(kq) : -1;  // -1 never matches a variable
-                        qj[t] = on ? key_j(kq) : -1;
-                        ptr[t] = on ? qbase[qv[t]] - c0 : 0u;
-                        fut[t] = 0.0;
-                    }
-                    for (int s = 0; s < m; ++s) {
-                        const u32 kk = ks[s];
-                        const int si = key_i(kk), sj = key_j(kk);
-                        const u16 cs = c[s];
-                        const double wd = double(int(cs) - 1);
-                        const double wb = wbt[cs];
-#pragma unroll
-                        for (int t = 0; t < K; ++t) {
-                            const bool self = s == qv[t];
-                            const bool inter = !self && ((si == qi[t]) | (si == qj[t]) | (sj == qi[t]) | (sj == qj[t]));
-                            double add = self ? 0.0 : wd;  // q itself is skipped (fut + 0.0 == fut)
-                            if (inter) {
-                                add = ((coin[ptr[t] >> 5] >> (ptr[t] & 31u)) & 1u) ? wb : 0.0;
-                                ++ptr[t];
-                            }
-                            fut[t] = __dadd_rn(fut[t], add);
+                if (!use_approx) {
+                    const double2 r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
+                    best_s = r.x;
+                    best_q = __double_lo_as_int(r.y);
+                } else {
+                    double lb = -INFINITY, h1 = 0.0, h2 = 0.0;
+                    int q1 = -1, q2 = -1;
+                    bool ovf = false;
+                    for (int qb = q_lo; qb < q_hi;) {
+                        if (q_hi - qb > NT) {
+                            gi_pass<2>(qb + tid, q_hi, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+                            qb += 2 * NT;
+                        } else {
+                            gi_pass<1>(qb + tid, q_hi, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+                            qb += NT;
                         }
                     }
-#pragma unroll
-                    for (int t = 0; t < K; ++t)
-                        if (qv[t] < q_hi) {
-                            const double h = __dadd_rn(double(int(c[qv[t]]) - 1), __dmul_rn(alpha, fut[t]));
-                            if (h > best_s || best_q == 0x7fffffff) {
-                                best_s = h;
-                                best_q = qv[t];
+                    B = fmax(B, block_max_d(lb));
+                    const double thr = __dsub_rn(B, eps2);
+                    const bool k1 = q1 >= 0 && h1 >= thr, k2 = q2 >= 0 && h2 >= thr;
+                    const u32 ns = u32(k1) + u32(k2);
+                    u32 info = (ovf ? 0x10000u : 0u) + ns;
+                    info = block_sum<NT>(info, red());
+                    if (info >> 16) {
+                        const double2 r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
+                        best_s = r.x;
+                        best_q = __double_lo_as_int(r.y);
+                    } else if ((info & 0xffffu) == 1u && q_lo == 0 && q_hi == m) {
+                        // a lone near-best candidate is the reference's pick
+                        if (k1)
+                            gi_keep(h1, q1, best_s, best_q);
+                        if (k2)
+                            gi_keep(h2, q2, best_s, best_q);
+                    } else {
+                        // fold every near-best candidate exactly, one warp each
+#pragma unroll 1
+                        for (int r = 0; r < 2; ++r) {
+                            const bool mine = r == 0 ? k1 : k2;
+                            const int qm = r == 0 ? q1 : q2;
+                            u32 pend = __ballot_sync(FULLMASK, mine);
+                            while (pend) {
+                                const int src = __ffs(pend) - 1;
+                                pend &= pend - 1;
+                                const int qf = __shfl_sync(FULLMASK, qm, src);
+                                gi_keep(gi_fold_dense(ks, c, m, qf, c0, alpha, topmin), qf, best_s, best_q);
                             }
                         }
+                    }
                 }
                 __syncthreads();
                 q_lo = q_hi;
@@ -1075,6 +1164,171 @@ struct St {
         }
         // @region gi_argmax
         return argmax(best_s, best_q);
+    }
+
+    __device__ __forceinline__ u32 wp_total() { return sp<u32>(lay.wp)[m]; }
+
+    // score_intersections_from's loop for candidates [q_lo, q_hi) of the
+    // current coin chunk; each thread carries up to K candidates through one
+    // pass (K independent double chains); first maximum kept per thread.
+    // Static and out of line: a cold path (prune off, negative beta, chunk
+    // overflow) that must not pull the process state into local memory.
+    static __device__ __noinline__ double2 gi_dense_chunk(const u32* ks, const u16* c, int m_, int q_lo, int q_hi,
+                                                          u32 c0, double alpha, double best_s, int best_q) {
+        constexpr int K = 3;
+        const u32* qbase = sp<u32>(lay.qbase);
+        const double* wbt = sp<double>(lay.wbt);
+        const u32* coin = sp<u32>(lay.coin);
+        for (int q0 = q_lo + int(threadIdx.x); q0 < q_hi; q0 += K * NT) {
+            int qv[K], qi[K], qj[K];
+            u32 ptr[K];
+            double fut[K];
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+                qv[t] = q0 + t * NT;
+                const bool on = qv[t] < q_hi;
+                const u32 kq = on ? ks[qv[t]] : 0u;
+                qi[t] = on ? key_i(kq) : -1;  // -1 never matches a variable
+                qj[t] = on ? key_j(kq) : -1;
+                ptr[t] = on ? qbase[qv[t]] - c0 : 0u;
+                fut[t] = 0.0;
+            }
+            for (int s = 0; s < m_; ++s) {
+                const u32 kk = ks[s];
+                const int si = key_i(kk), sj = key_j(kk);
+                const u16 cs = c[s];
+                const double wd = double(int(cs) - 1);
+                const double wb = wbt[cs];
+#pragma unroll
+                for (int t = 0; t < K; ++t) {
+                    const bool self = s == qv[t];
+                    const bool inter = !self && ((si == qi[t]) | (si == qj[t]) | (sj == qi[t]) | (sj == qj[t]));
+                    double add = self ? 0.0 : wd;  // q itself is skipped (fut + 0.0 == fut)
+                    if (inter) {
+                        add = ((coin[ptr[t] >> 5] >> (ptr[t] & 31u)) & 1u) ? wb : 0.0;
+                        ++ptr[t];
+                    }
+                    fut[t] = __dadd_rn(fut[t], add);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < K; ++t)
+                if (qv[t] < q_hi)
+                    gi_keep(__dadd_rn(double(int(c[qv[t]]) - 1), __dmul_rn(alpha, fut[t])), qv[t], best_s, best_q);
+        }
+        return make_double2(best_s, __int_as_double_lo(best_q));
+    }
+
+    // Approximate gi scores of candidates q0, q0 + NT, ..., q0 + (K-1) NT
+    // (< q_hi): exact integer sums over the list, packed A = I << 16 | C with
+    // I = intersecting weight, C = its coin-selected part (T < 2^16 on this
+    // path).  A candidate's coins (at most 64 on this path) sit in a 64-bit
+    // window consumed one bit per intersecting candidate.  Near-best
+    // bookkeeping as in the walk's approximate pass.
+    template <int K>
+    __device__ __forceinline__ void gi_pass(int q0, int q_hi, u32 c0, u32 T, double alpha, double beta, double eps2,
+                                            double& lb, int& q1, double& h1, int& q2, double& h2, bool& ovf) {
+        const u32* ks = keys();
+        const u16* c = cnts();
+        const u32* qbase = sp<u32>(lay.qbase);
+        const u32* coin = sp<u32>(lay.coin);
+        int qv[K], qi[K], qj[K];
+        u32 lo[K], hi[K], A[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            qv[t] = q0 + t * NT;
+            const bool on = qv[t] < q_hi;
+            const u32 kq = on ? ks[qv[t]] : 0u;
+            qi[t] = on ? key_i(kq) : -1;  // -1 never matches a variable
+            qj[t] = on ? key_j(kq) : -1;
+            const u32 p = on ? qbase[qv[t]] - c0 : 0u;
+            const u32 w0 = coin[p >> 5], w1 = coin[(p >> 5) + 1], w2 = coin[(p >> 5) + 2];
+            lo[t] = __funnelshift_r(w0, w1, p & 31u);
+            hi[t] = __funnelshift_r(w1, w2, p & 31u);
+            A[t] = 0u;
+        }
+        const int m_ = m;
+#pragma unroll 2
+        for (int s = 0; s < m_; ++s) {
+            const u32 kk = ks[s];
+            const int si = key_i(kk), sj = key_j(kk);
+            const u32 w = u32(c[s]) - 1u;
+            const u32 wI = w << 16, wC = wI | w;
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+                const bool inter = (s != qv[t]) & ((si == qi[t]) | (si == qj[t]) | (sj == qi[t]) | (sj == qj[t]));
+                if (inter) {
+                    A[t] += (lo[t] & 1u) ? wC : wI;
+                    lo[t] = __funnelshift_r(lo[t], hi[t], 1);
+                    hi[t] >>= 1;
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            if (qv[t] >= q_hi)
+                continue;
+            const u32 wq = u32(c[qv[t]]) - 1u;
+            const double F = __dadd_rn(double(T - wq - (A[t] >> 16)), __dmul_rn(beta, double(A[t] & 0xffffu)));
+            const double h = __dadd_rn(double(wq), __dmul_rn(alpha, F));
+            lb = fmax(lb, h);
+            const double lim = __dsub_rn(lb, eps2);
+            if (q1 >= 0 && h1 < lim)
+                q1 = -1;
+            if (q2 >= 0 && h2 < lim)
+                q2 = -1;
+            if (h >= lim) {
+                if (q1 < 0) {
+                    q1 = qv[t];
+                    h1 = h;
+                } else if (q2 < 0) {
+                    q2 = qv[t];
+                    h2 = h;
+                } else {
+                    ovf = true;
+                }
+            }
+        }
+    }
+
+    // exact gi score of q (score_intersections_from's sequential sum) on the
+    // dense layout, by one whole warp: q's intersecting candidates come from
+    // ballots over the list in canonical order, runs of disjoint candidates
+    // are added in O(1) by add_run.  Warp-uniform q, result on every lane.
+    static __device__ __noinline__ double gi_fold_dense(const u32* ks, const u16* c, int m_, int q, u32 c0,
+                                                       double alpha, double topmin) {
+        const u32* coin = sp<u32>(lay.coin);
+        const u32* wp = sp<u32>(lay.wp);
+        const double* wbt = sp<double>(lay.wbt);
+        const int lane = int(threadIdx.x & 31);
+        const u32 kq = ks[q];
+        const int qi = key_i(kq), qj = key_j(kq);
+        u32 ptr = sp<u32>(lay.qbase)[q] - c0;
+        double f = 0.0;
+        int prev = 0;
+        for (int base = 0; base < m_; base += 32) {
+            const int s = base + lane;
+            bool hit = false;
+            if (s < m_) {
+                const u32 kk = ks[s];
+                const int si = key_i(kk), sj = key_j(kk);
+                hit = (si == qi) | (si == qj) | (sj == qi) | (sj == qj);  // q itself included
+            }
+            u32 msk = __ballot_sync(FULLMASK, hit);
+            while (msk) {
+                const int s2 = base + __ffs(msk) - 1;
+                msk &= msk - 1;
+                f = add_run(f, prev, s2, wp, topmin);
+                prev = s2 + 1;
+                if (s2 != q) {
+                    if ((coin[ptr >> 5] >> (ptr & 31u)) & 1u)
+                        f = __dadd_rn(f, wbt[c[s2]]);
+                    ++ptr;
+                }
+            }
+        }
+        f = add_run(f, prev, m_, wp, topmin);
+        return __dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, f));
     }
 
     __device__ __forceinline__ static void gi_keep(double h, int q, double& best_s, int& best_q) {
@@ -1195,7 +1449,7 @@ struct St {
     // which element crosses — as long as no single element can skip a binade
     // (top >= topmin = max w + 1): then the crossing is done in O(1).  Below
     // that the crossing element is located by binary search in wp.
-    __device__ __forceinline__ double add_run(double f, int L, int R, const u32* wp, double topmin) {
+    static __device__ __forceinline__ double add_run(double f, int L, int R, const u32* wp, double topmin) {
         u32 tot = wp[R] - wp[L];
         while (tot != 0u) {
             if (f == trunc(f))

@@ -1,9 +1,10 @@
 """Both exact Greedy-Intersections forms against the oracle (search.cu
-sel_gi / add_run): the dense reference loop (TCSE_GI_DENSE=1) and the O(deg)
-walk (TCSE_GI_DENSE=0), forced on the same processes — the walk both with
-near-best pruning (default: approximate scores from exact integer sums, exact
-folds only within the rounding bound of the best) and folding every candidate
-(TCSE_GI_PRUNE=0).
+sel_gi / add_run): the dense layout (TCSE_GI_DENSE=1) and the O(deg) walk
+(TCSE_GI_DENSE=0), forced on the same processes — each both with near-best
+pruning (default: approximate scores from exact integer sums, exact folds only
+within the rounding bound of the best; dense: gi_pass + gi_fold_dense) and
+without it (TCSE_GI_PRUNE=0: the walk folds every candidate, the dense layout
+runs the reference loop itself).
 
 The walk adds runs of disjoint candidates in O(1), including the binade
 crossings of the running double sum: by binary search below max(c-1)+1 and
@@ -65,7 +66,7 @@ def systems(rng):
     return out
 
 
-@pytest.mark.parametrize("form", ["1", "0", "0-exact"])
+@pytest.mark.parametrize("form", ["1", "1-exact", "0", "0-exact"])
 def test_gi_forms_match_oracle(dev, monkeypatch, form):
     monkeypatch.setenv("TCSE_GI_DENSE", form[0])
     monkeypatch.setenv("TCSE_GI_PRUNE", "0" if form.endswith("exact") else "1")
