@@ -1029,7 +1029,7 @@ struct St {
                 // @region gi_approx_pass
                 if (!gi_prune) {
                     for (int q = q_lo + tid; q < q_hi; q += NT) {
-                        const double h = gi_fold(q, c0, alpha, topmin);
+                        const double h = gi_fold(ks, c, m, q, c0, alpha, topmin);
                         if (h > best_s || best_q == 0x7fffffff) {
                             best_s = h;
                             best_q = q;
@@ -1040,7 +1040,7 @@ struct St {
                     int q1 = -1, q2 = -1;
                     bool ovf = false;
                     for (int q = q_lo + tid; q < q_hi; q += NT) {
-                        const double h = gi_approx(q, c0, T, alpha, beta);
+                        const double h = gi_approx(ks, c, q, c0, T, alpha, beta);
                         lb = fmax(lb, h);
                         const double lim = __dsub_rn(lb, eps2);
                         if (q1 >= 0 && h1 < lim)
@@ -1063,12 +1063,15 @@ struct St {
                     B = fmax(B, block_max_d(lb));
                     const double thr = __dsub_rn(B, eps2);
                     if (ovf) {  // more than two near-ties in one thread: rescan
-                        gi_rescan(q_lo, q_hi, c0, T, alpha, beta, topmin, thr, best_s, best_q);
+                        const double2 r = gi_rescan(ks, c, m, q_lo, q_hi, c0, T, alpha, beta, topmin, thr, best_s,
+                                                    best_q);
+                        best_s = r.x;
+                        best_q = __double_lo_as_int(r.y);
                     } else {
                         if (q1 >= 0 && h1 >= thr)
-                            gi_keep(gi_fold(q1, c0, alpha, topmin), q1, best_s, best_q);
+                            gi_keep(gi_fold(ks, c, m, q1, c0, alpha, topmin), q1, best_s, best_q);
                         if (q2 >= 0 && h2 >= thr)
-                            gi_keep(gi_fold(q2, c0, alpha, topmin), q2, best_s, best_q);
+                            gi_keep(gi_fold(ks, c, m, q2, c0, alpha, topmin), q2, best_s, best_q);
                     }
                 }
                 __syncthreads();
@@ -1363,8 +1366,8 @@ struct St {
     // second, by index; then the contiguous run holding it first).  q itself
     // and its opposite-sign twin appear in both and are visited once.
     template <typename F>
-    __device__ __forceinline__ void gi_neighbours(int q, F&& visit) {
-        const u32 kq = keys()[q];
+    static __device__ __forceinline__ void gi_neighbours(const u32* ks, int q, F&& visit) {
+        const u32 kq = ks[q];
         const int qi = key_i(kq), qj = key_j(kq);
         const u32* aoff = sp<u32>(lay.aoff);
         const u32* nA = sp<u32>(lay.nA);
@@ -1386,12 +1389,12 @@ struct St {
     }
 
     // approximate gi score of q: exact integer sums, three roundings
-    __device__ __forceinline__ double gi_approx(int q, u32 c0, u32 T, double alpha, double beta) {
-        const u16* c = cnts();
+    static __device__ __forceinline__ double gi_approx(const u32* ks, const u16* c, int q, u32 c0, u32 T,
+                                                       double alpha, double beta) {
         const u32* coin = sp<u32>(lay.coin);
         u32 ptr = sp<u32>(lay.qbase)[q] - c0;
         u32 I = 0, C = 0;
-        gi_neighbours(q, [&](int s) {
+        gi_neighbours(ks, q, [&](int s) {
             if (s == 0x7fffffff)
                 return false;
             if (s != q) {
@@ -1407,25 +1410,26 @@ struct St {
         return __dadd_rn(double(wq), __dmul_rn(alpha, F));
     }
 
-    __device__ __noinline__ void gi_rescan(int q_lo, int q_hi, u32 c0, u32 T, double alpha, double beta,
-                                           double topmin, double thr, double& best_s, int& best_q) {
-        for (int q = q_lo + tid; q < q_hi; q += NT)
-            if (gi_approx(q, c0, T, alpha, beta) >= thr)
-                gi_keep(gi_fold(q, c0, alpha, topmin), q, best_s, best_q);
+    static __device__ __noinline__ double2 gi_rescan(const u32* ks, const u16* c, int m_, int q_lo, int q_hi, u32 c0,
+                                                     u32 T, double alpha, double beta, double topmin, double thr,
+                                                     double best_s, int best_q) {
+        for (int q = q_lo + int(threadIdx.x); q < q_hi; q += NT)
+            if (gi_approx(ks, c, q, c0, T, alpha, beta) >= thr)
+                gi_keep(gi_fold(ks, c, m_, q, c0, alpha, topmin), q, best_s, best_q);
+        return make_double2(best_s, __int_as_double_lo(best_q));
     }
 
     // exact gi score of q: score_intersections_from's sequential sum, runs of
     // disjoint candidates added in O(1) by add_run
-    __device__ __noinline__ double gi_fold(int q, u32 c0, double alpha, double topmin) {
-        const u16* c = cnts();
+    static __device__ __noinline__ double gi_fold(const u32* ks, const u16* c, int m_, int q, u32 c0, double alpha,
+                                                  double topmin) {
         const u32* coin = sp<u32>(lay.coin);
         const u32* wp = sp<u32>(lay.wp);
         const double* wbt = sp<double>(lay.wbt);
-        const int m_ = m;
         u32 ptr = sp<u32>(lay.qbase)[q] - c0;
         double f = 0.0;
         int prev = 0;
-        gi_neighbours(q, [&](int s) {
+        gi_neighbours(ks, q, [&](int s) {
             f = add_run(f, prev, s == 0x7fffffff ? m_ : s, wp, topmin);
             if (s == 0x7fffffff)
                 return false;
