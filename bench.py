@@ -410,7 +410,9 @@ def main():
                      "kernel": "search_kernel<W=1,NT=64>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms),
                      "ncu_issue": issue},
         "clocks": clk,
-        "gpu_launches": int(3 * args.steps),  # prep + search + reduce per iteration
+        # per search launch (one per launch group) prep + place + search, per
+        # iteration pack + reduce
+        "gpu_launches": int(3 * launches + 2 * args.steps),
         "substitution_steps": int(steps_all),
         "incumbent_costs": [r.cost for r, _ in results],
     }
