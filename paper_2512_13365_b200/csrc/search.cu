@@ -626,15 +626,22 @@ struct St {
         u16* ncn = sp<u16>(lay.ncn);
         u32* aux = sp<u32>(lay.aux);
         u32* newexcl = sp<u32>(lay.newexcl);
-        // (a) recount old candidates touching i or j (their counts only drop)
+        // (a) recount old candidates touching i or j (their counts only drop);
+        // blocked ranges, survivors counted on the way
+        const int Em = (m + NT - 1) / NT;
+        const int a0 = min(m, tid * Em), a1 = min(m, a0 + Em);
+        u32 keep = 0;
 #pragma unroll 1
-        for (int t = tid; t < m; t += NT) {
+        for (int t = a0; t < a1; ++t) {
             const u32 kk = ok[t];
             const int a = key_i(kk), b = key_j(kk);
-            tcnt[t] = (a == i || a == j || b == i || b == j) ? u16(count_pair<W>(a, b, key_neg(kk))) : oc[t];
+            const u16 ct = (a == i || a == j || b == i || b == j) ? u16(count_pair<W>(a, b, key_neg(kk))) : oc[t];
+            tcnt[t] = ct;
+            keep += ct >= 2 ? 1u : 0u;
         }
         // (b) the new variable's pairs (x, k, +/-)
         const u64* pk = P(k - 1);
+        bool anynew = false;
         u64 kp[W], kn[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) {
@@ -652,8 +659,26 @@ struct St {
             }
             ncp[x] = u16(cp);
             ncn[x] = u16(cn);
+            anynew |= (cp >= 2) | (cn >= 2);
         }
-        __syncthreads();
+        if (!__syncthreads_or(anynew)) {
+            // common case: no pair with k repeats, the list only loses entries
+            const u64 sc = block_scan_ool<NT>(keep, red());
+            u32* dk = sp<u32>(cur ? lay.keys0 : lay.keys1);
+            u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
+            u32 o = u32(sc);
+#pragma unroll 1
+            for (int t = a0; t < a1; ++t)
+                if (tcnt[t] >= 2) {
+                    dk[o] = ok[t];
+                    dc[o] = tcnt[t];
+                    ++o;
+                }
+            __syncthreads();
+            cur ^= 1;
+            m = int(sc >> 32);
+            return true;
+        }
         // (c) one packed scan: low 16 bits old survivors, high 16 bits new pairs
         const int L = m + 2 * (k - 1);
         const int E = (L + NT - 1) / NT;
