@@ -197,7 +197,7 @@ __device__ __forceinline__ u32 block_sum(u32 v, u32* red) {
 // (-inf, 0x7fffffff), so any real score beats them (scores can be negative
 // for user alpha/beta)
 template <int NT>
-__device__ __noinline__ int block_argmax_double(double s, int idx, double* reds, int* redi) {
+__device__ __forceinline__ int block_argmax_double(double s, int idx, double* reds, int* redi) {
     constexpr int NW = NT / 32;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1616,7 +1616,7 @@ __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) 
 // shared memory unless the kernel is held to ~64 registers at 128 threads.
 template <int NT>
 struct MinBlocks {
-    static constexpr int value = NT == 32 ? 32 : (NT == 64 ? 16 : (NT == 128 ? 8 : 4));
+    static constexpr int value = NT == 32 ? 28 : (NT == 64 ? 14 : (NT == 128 ? 8 : 4));
 };
 
 template <int W, int NT, bool GID>
