@@ -398,7 +398,12 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.words = d.h.w_need;
     sd.coin_words = coin_words_for(d.h);
     sd.gi_dense = d.dense ? 1 : 0;
-    sd.gi_prune = env_int("TCSE_GI_PRUNE", 1);
+    // near-best pruning pays once candidate lists are long enough that the
+    // O(m^2) scoring outweighs its extra reductions and tie folds: on for
+    // systems starting above 32 candidates (laderman-size systems, with
+    // frequent exact ties, run the reference loop; sweep
+    // scripts/prune_threshold.sh).  TCSE_GI_PRUNE=k forces k (0 = off).
+    sd.gi_prune = env_int("TCSE_GI_PRUNE", d.base_m > 32 ? 1 : 0);
     sd.vcap = d.h.vcap;
     sd.mcap = d.h.mcap;
     sd.sub_cap = d.h.naive / 2 + 1;

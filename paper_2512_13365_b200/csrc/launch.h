@@ -40,7 +40,7 @@ struct SysDesc {
     int32_t words;    // ceil(n_e / 64): words a mask needs (the launch may use more)
     int32_t coin_words;  // gi coin buffer (u32 words) per block
     int32_t gi_dense;    // 1: gi by the reference's O(m) loop per candidate; 0: O(deg) walk
-    int32_t gi_prune;    // walk: exact folds only for near-best approximate scores (0: fold all)
+    int32_t gi_prune;    // > 0: near-best pruning (walk: exact folds only near the best; dense: from gi_prune candidates on); 0: off
     int32_t vcap;     // variable capacity = n_x + naive
     int32_t mcap;     // candidate capacity (<= pair occurrences / 2)
     int32_t sub_cap;  // record stride (u32 keys) = naive + 1

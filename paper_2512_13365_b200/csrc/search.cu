@@ -102,6 +102,15 @@ __device__ __forceinline__ double uniform_real(u64 x, double a, double b) {
 
 __shared__ Lay lay;
 
+#ifdef TCSE_GI_STATS
+// debug build only: gi path counters (approx steps, lone picks, folds,
+// overflow fallbacks, reference-loop steps, sum of m, multi-survivor steps)
+__device__ unsigned long long g_gi_stats[8];
+#define GI_STAT(k, v) do { if (threadIdx.x == 0) atomicAdd(&g_gi_stats[k], (unsigned long long)(v)); } while (0)
+#else
+#define GI_STAT(k, v) do { } while (0)
+#endif
+
 __device__ __forceinline__ double __int_as_double_lo(int v) { return __hiloint2double(0, v); }
 __device__ __forceinline__ int __double_lo_as_int(double d) { return __double2loint(d); }
 
@@ -852,7 +861,7 @@ struct St {
         const bool walk = !dense && beta >= 0.0;
         // dense form with near-best pruning: integer score sums in the
         // candidate loop, exact folds only for near-ties (same bound as the walk)
-        const bool approx = dense && gi_prune && beta >= 0.0;
+        const bool approx = dense && gi_prune > 0 && m >= gi_prune && beta >= 0.0;
         // max c - 1 over the list (crossing bound) and max coins per candidate
         // in wbt's spare slot
         u32* s_wmax = reinterpret_cast<u32*>(sp<double>(lay.wbt) + sd_ne + 1);
@@ -1138,6 +1147,7 @@ struct St {
                 const int q_hi = lo;
                 draw_coins(qbase[q_hi] - c0);
                 if (!use_approx) {
+                    GI_STAT(4, 1);
                     const double2 r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
                     best_s = r.x;
                     best_q = __double_lo_as_int(r.y);
@@ -1160,18 +1170,24 @@ struct St {
                     const u32 ns = u32(k1) + u32(k2);
                     u32 info = (ovf ? 0x10000u : 0u) + ns;
                     info = block_sum<NT>(info, red());
+                    GI_STAT(0, 1);
+                    GI_STAT(5, m);
                     if (info >> 16) {
+                        GI_STAT(3, 1);
                         const double2 r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
                         best_s = r.x;
                         best_q = __double_lo_as_int(r.y);
                     } else if ((info & 0xffffu) == 1u && q_lo == 0 && q_hi == m) {
                         // a lone near-best candidate is the reference's pick
+                        GI_STAT(1, 1);
                         if (k1)
                             gi_keep(h1, q1, best_s, best_q);
                         if (k2)
                             gi_keep(h2, q2, best_s, best_q);
                     } else {
                         // fold every near-best candidate exactly, one warp each
+                        GI_STAT(6, 1);
+                        GI_STAT(2, info & 0xffffu);
 #pragma unroll 1
                         for (int r = 0; r < 2; ++r) {
                             const bool mine = r == 0 ? k1 : k2;
@@ -1201,9 +1217,9 @@ struct St {
     // pass (K independent double chains); first maximum kept per thread.
     // Static and out of line: a cold path (prune off, negative beta, chunk
     // overflow) that must not pull the process state into local memory.
-    static __device__ __noinline__ double2 gi_dense_chunk(const u32* ks, const u16* c, int m_, int q_lo, int q_hi,
-                                                          u32 c0, double alpha, double best_s, int best_q) {
-        constexpr int K = 3;
+    template <int K>
+    static __device__ __forceinline__ double2 gi_dense_chunk_k(const u32* ks, const u16* c, int m_, int q_lo, int q_hi,
+                                                               u32 c0, double alpha, double best_s, int best_q) {
         const u32* qbase = sp<u32>(lay.qbase);
         const double* wbt = sp<double>(lay.wbt);
         const u32* coin = sp<u32>(lay.coin);
@@ -1245,6 +1261,14 @@ struct St {
                     gi_keep(__dadd_rn(double(int(c[qv[t]]) - 1), __dmul_rn(alpha, fut[t])), qv[t], best_s, best_q);
         }
         return make_double2(best_s, __int_as_double_lo(best_q));
+    }
+
+    // K = 1 when the chunk fits one candidate per thread (no idle chains)
+    static __device__ __noinline__ double2 gi_dense_chunk(const u32* ks, const u16* c, int m_, int q_lo, int q_hi,
+                                                          u32 c0, double alpha, double best_s, int best_q) {
+        if (q_hi - q_lo <= NT)
+            return gi_dense_chunk_k<1>(ks, c, m_, q_lo, q_hi, c0, alpha, best_s, best_q);
+        return gi_dense_chunk_k<3>(ks, c, m_, q_lo, q_hi, c0, alpha, best_s, best_q);
     }
 
     // Approximate gi scores of candidates q0, q0 + NT, ..., q0 + (K-1) NT
@@ -1582,7 +1606,7 @@ struct St {
     }
 
     int sd_ne;
-    int gi_prune;  // 0: fold every candidate exactly (test hook)
+    int gi_prune;  // 0: no pruning (test hook); dense layout: prune from this many candidates on
     int mcap;  // candidate capacity of the layout
 };
 
@@ -2165,3 +2189,15 @@ cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st) {
 int search_smem_attr_max() { return 227 * 1024; }
 
 }  // namespace tcse
+
+#ifdef TCSE_GI_STATS
+extern "C" int tcse_debug_gi_stats(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, tcse::g_gi_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(tcse::g_gi_stats, z, sizeof z);
+    }
+    return 0;
+}
+#endif

@@ -8,3 +8,6 @@ timeout 400 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${tag}_ncu_bench.log 2>&1
 bash scripts/ncu_ab.sh "${tag}_search:cur:X=1"
+if [ -n "$ALLCFG" ]; then
+  for c in 0 1 3 4; do timeout 600 python bench.py --config $c > gpurun_out/${tag}_bench_cfg$c.json 2> gpurun_out/${tag}_bench_cfg$c.err; done
+fi
