@@ -11,3 +11,6 @@ bash scripts/ncu_ab.sh "${tag}_search:cur:X=1"
 if [ -n "$ALLCFG" ]; then
   for c in 0 1 3 4; do timeout 600 python bench.py --config $c > gpurun_out/${tag}_bench_cfg$c.json 2> gpurun_out/${tag}_bench_cfg$c.err; done
 fi
+if [ -n "$WALL" ]; then
+  timeout 900 python scripts/wall_budget.py > gpurun_out/${tag}_wall_budget.log 2>&1
+fi
