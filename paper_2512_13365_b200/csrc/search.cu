@@ -62,7 +62,7 @@ constexpr u64 kMtA = 0xb5026f5aa96619e9ULL;
 constexpr u64 kMtF = 6364136223846793005ULL;
 // top bit of the tempered output = parity of these raw state bits
 #ifndef TCSE_FUSED_TWIST_MIN
-#define TCSE_FUSED_TWIST_MIN 128  // block sizes that twist in one fused two-barrier pass
+#define TCSE_FUSED_TWIST_MIN 128  // block sizes whose coin generations run register-resident (mt_coin_run)
 #endif
 constexpr u64 kCoinMask = 0x8080000004000200ULL;
 
@@ -341,6 +341,118 @@ __device__ __noinline__ void mt_twist_small() {
     __syncthreads();
 }
 
+// Coins from consecutive fresh mt19937_64 generations with the state held in
+// registers (precondition: every output of the current generation consumed).
+// Element i < 156 of the state is the pair (lo = mt[i], hi = mt[i + 156]),
+// in lane i % 32 of group i / 32 (groups round-robin over the warps).  One
+// twist: new lo[i] = mix(lo[i], lo[i+1], hi[i]), new hi[i] = mix(hi[i],
+// hi[i+1], new lo[i]), with old[312] := new[0] for i = 155 — neighbours come
+// by shuffle within a group and from the previous twist's published group
+// boundaries (double-buffered) across groups, so a generation costs one
+// barrier (none for one-warp blocks) instead of the smem twist's two to five.
+// Output e of generation t is coin pos0 + 312 t + e (tempered top bit =
+// parity of raw bits {63, 55, 26, 9}).  Writes the last generation back to
+// smem and returns how many of its outputs were taken.
+template <int NT>
+__device__ __noinline__ u32 mt_coin_run(u32* coin, u32 pos0, u32 nbits) {
+    constexpr int NW = NT / 32;
+    constexpr int RG = (5 + NW - 1) / NW;  // groups per warp
+    __shared__ u64 bnd[2][12];             // per group (lo, hi) of lane 0, + lo of element 1
+    u64* mt = sp<u64>(lay.mt);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u64 lo[RG], hi[RG];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+        const int g = warp + r * NW;
+        const int i = 32 * g + lane;
+        lo[r] = 0ULL;
+        hi[r] = 0ULL;
+        if (g < 5 && i < 156) {
+            lo[r] = mt[i];
+            hi[r] = mt[i + 156];
+            if (lane == 0) {
+                bnd[0][2 * g] = lo[r];
+                bnd[0][2 * g + 1] = hi[r];
+            }
+            if (i == 1)
+                bnd[0][10] = lo[r];
+        }
+    }
+    if (NW > 1)
+        __syncthreads();
+    else
+        __syncwarp();
+    const u32 T = (nbits + 311) / 312;
+    u32 n_t = 0;
+#pragma unroll 1
+    for (u32 t = 0; t < T; ++t) {
+        const int b = int(t & 1u);
+        n_t = min(312u, nbits - 312u * t);
+        const u32 base = pos0 + 312u * t;
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+            const int g = warp + r * NW;
+            if (g >= 5)  // warp-uniform
+                continue;
+            const int i = 32 * g + lane;
+            u64 nlo = __shfl_down_sync(FULLMASK, lo[r], 1);
+            u64 nhi = __shfl_down_sync(FULLMASK, hi[r], 1);
+            if (lane == 31 && g < 4) {
+                nlo = bnd[b][2 * g + 2];
+                nhi = bnd[b][2 * g + 3];
+            }
+            if (i == 155) {
+                nlo = bnd[b][1];                                     // old[156]
+                nhi = mt_mix(bnd[b][0], bnd[b][10], bnd[b][1]);      // old[312] := new[0]
+            }
+            const u64 l2 = mt_mix(lo[r], nlo, hi[r]);
+            const u64 h2 = mt_mix(hi[r], nhi, l2);
+            lo[r] = l2;
+            hi[r] = h2;
+            const bool ok = i < 156;
+            const u32 blo = (ok && u32(i) < n_t) ? (u32(__popcll(l2 & kCoinMask)) & 1u) : 0u;
+            const u32 bhi = (ok && u32(i) + 156u < n_t) ? (u32(__popcll(h2 & kCoinMask)) & 1u) : 0u;
+            const u32 balo = __ballot_sync(FULLMASK, blo);
+            const u32 bahi = __ballot_sync(FULLMASK, bhi);
+            if (lane == 0) {
+                if (balo) {
+                    const u32 pos = base + 32u * u32(g);
+                    const u32 w0 = pos >> 5, sh = pos & 31;
+                    atomicOr(&coin[w0], balo << sh);
+                    if (sh)
+                        atomicOr(&coin[w0 + 1], balo >> (32 - sh));
+                }
+                if (bahi) {
+                    const u32 pos = base + 156u + 32u * u32(g);
+                    const u32 w0 = pos >> 5, sh = pos & 31;
+                    atomicOr(&coin[w0], bahi << sh);
+                    if (sh)
+                        atomicOr(&coin[w0 + 1], bahi >> (32 - sh));
+                }
+                bnd[b ^ 1][2 * g] = l2;
+                bnd[b ^ 1][2 * g + 1] = h2;
+            }
+            if (i == 1)
+                bnd[b ^ 1][10] = l2;
+        }
+        if (NW > 1)
+            __syncthreads();
+        else
+            __syncwarp();
+    }
+#pragma unroll
+    for (int r = 0; r < RG; ++r) {
+        const int g = warp + r * NW;
+        const int i = 32 * g + lane;
+        if (g < 5 && i < 156) {
+            mt[i] = lo[r];
+            mt[i + 156] = hi[r];
+        }
+    }
+    __syncthreads();
+    return n_t;
+}
+
 template <int NT>
 __device__ __forceinline__ void mt_twist() {
     if constexpr (NT >= TCSE_FUSED_TWIST_MIN)
@@ -548,12 +660,10 @@ struct St {
         while (done < nbits) {
             if (mti >= 312) {
                 if constexpr (NT >= TCSE_FUSED_TWIST_MIN) {
-                    // fresh generation: twist and take its first n outputs in one pass
-                    const u32 n = min(312u, nbits - done);
-                    mt_twist_impl<NT, true>(coin, done, n);
-                    mti = int(n);
-                    done += n;
-                    continue;
+                    // every remaining coin from fresh generations, state in registers
+                    mti = int(mt_coin_run<NT>(coin, done, nbits - done));
+                    done = nbits;
+                    break;
                 } else {
                     mt_twist<NT>();
                     mti = 0;
