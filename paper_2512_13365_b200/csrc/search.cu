@@ -1785,10 +1785,18 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             }
         }
         if (s_slot.rng) {
+            // all loads in flight before the stores (2.5 KB from HBM per process)
+            constexpr int R = (312 + NT - 1) / NT;
             u64* mt = sp<u64>(lay.mt);
             const u64* src = L.rng + size_t(blk) * 312;
-            for (int t = tid; t < 312; t += NT)
-                mt[t] = src[t];
+            u64 v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                v[r] = tid + r * NT < 312 ? __ldg(src + tid + r * NT) : 0ULL;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (tid + r * NT < 312)
+                    mt[tid + r * NT] = v[r];
         }
     }
     __syncthreads();
@@ -1836,57 +1844,14 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     u32* rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
     u64* trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
     const bool dump = sd.mode == kModeDump;
-    int t_pre = 0, n_rec = 0, n_own = 0, step = 0;
+    int n_rec = 0, n_own = 0, step = 0;
     u64 wops = 0;
-    for (;;) {
-        u32 q;
-        const bool replay = t_pre < n_pre;
-        if (replay) {
-            q = pre[t_pre];
-            const int qi = key_i(q), qj = key_j(q);
-            if (qi < 1 || qj <= qi || qj > pr.V) {
-                set_error(sd, TCSE_EREPLAY, t_pre);
-                if (tid == 0 && sd.out_cost)
-                    sd.out_cost[lp] = -1;
-                return;
-            }
-        } else {
-            if (dump)
-                break;
-            if (trace && tid == 0 && step < sd.trace_stride)
-                trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
-            ++step;
-            if (pr.m == 0)
-                break;
-            int strat = strategy;
-            if (strat == TCSE_MIXED)
-                strat = pr.mixed_sub(s_mix);  // select_mixed (strategies.hpp:260-269)
-            if (strat == TCSE_GREEDY_RANDOM)  // select_greedy_random (119-124)
-                strat = uniform_real(pr.draw(), 0.0, 1.0) < p_greedy ? TCSE_GREEDY_ALTERNATIVE : TCSE_WEIGHTED_RANDOM;
-            if ((strat == TCSE_GREEDY_INTERSECTIONS || strat == TCSE_GREEDY_POTENTIAL) && alpha == 0.0)
-                strat = TCSE_GREEDY;  // gain only (strategies.hpp:140-141, 205-206)
-            const u64 Vt = u64(pr.V), mt_ = u64(pr.m), we = u64(sd.words);
-            int pick;
-            u64 sel = mt_;
-            if (strat == TCSE_GREEDY) {
-                pick = pr.sel_greedy();
-            } else if (strat == TCSE_GREEDY_ALTERNATIVE) {
-                pick = pr.sel_ga();
-            } else if (strat == TCSE_WEIGHTED_RANDOM) {
-                pick = pr.sel_wr();
-            } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
-                pick = pr.template sel_gi<GID>(alpha, beta);
-                sel += pr.last_coins;
-            } else {
-                pick = pr.sel_gp(alpha);
-                sel += mt_ * (Vt - 2) * 4 * we;
-            }
-            // recount 12(V-1)W_E + substitution 8 W_E + selection
-            wops += 12 * (Vt - 1) * we + 8 * we + sel;
-            q = pr.keys()[pick];
-        }
-        const int c = pr.apply(q);
-        if (c == 0) {  // only a replayed pair can be absent
+    // prefix replay (reinit from the incumbent, or a fixed replay): apply +
+    // update only, its own loop so the search loop carries no prefix state
+    for (int t_pre = 0; t_pre < n_pre; ++t_pre) {
+        const u32 q = pre[t_pre];
+        const int qi = key_i(q), qj = key_j(q);
+        if (qi < 1 || qj <= qi || qj > pr.V || pr.apply(q) == 0) {
             set_error(sd, TCSE_EREPLAY, t_pre);
             if (tid == 0 && sd.out_cost)
                 sd.out_cost[lp] = -1;
@@ -1896,13 +1861,54 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             set_error(sd, kErrCandOverflow, pr.m);
             return;
         }
-        if (replay) {
-            ++t_pre;
-            if (!rec_prefix)
-                continue;
-        } else {
-            ++n_own;
+        if (rec_prefix) {
+            if (tid == 0 && n_rec < sd.sub_cap)
+                rec[n_rec] = q;
+            ++n_rec;
+            if (n_rec > sd.sub_cap) {
+                set_error(sd, TCSE_ECAPACITY, n_rec);
+                return;
+            }
         }
+    }
+    while (!dump) {
+        if (trace && tid == 0 && step < sd.trace_stride)
+            trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
+        ++step;
+        if (pr.m == 0)
+            break;
+        int strat = strategy;
+        if (strat == TCSE_MIXED)
+            strat = pr.mixed_sub(s_mix);  // select_mixed (strategies.hpp:260-269)
+        if (strat == TCSE_GREEDY_RANDOM)  // select_greedy_random (119-124)
+            strat = uniform_real(pr.draw(), 0.0, 1.0) < p_greedy ? TCSE_GREEDY_ALTERNATIVE : TCSE_WEIGHTED_RANDOM;
+        if ((strat == TCSE_GREEDY_INTERSECTIONS || strat == TCSE_GREEDY_POTENTIAL) && alpha == 0.0)
+            strat = TCSE_GREEDY;  // gain only (strategies.hpp:140-141, 205-206)
+        const u64 Vt = u64(pr.V), mt_ = u64(pr.m), we = u64(sd.words);
+        int pick;
+        u64 sel = mt_;
+        if (strat == TCSE_GREEDY) {
+            pick = pr.sel_greedy();
+        } else if (strat == TCSE_GREEDY_ALTERNATIVE) {
+            pick = pr.sel_ga();
+        } else if (strat == TCSE_WEIGHTED_RANDOM) {
+            pick = pr.sel_wr();
+        } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
+            pick = pr.template sel_gi<GID>(alpha, beta);
+            sel += pr.last_coins;
+        } else {
+            pick = pr.sel_gp(alpha);
+            sel += mt_ * (Vt - 2) * 4 * we;
+        }
+        // recount 12(V-1)W_E + substitution 8 W_E + selection
+        wops += 12 * (Vt - 1) * we + 8 * we + sel;
+        const u32 q = pr.keys()[pick];
+        pr.apply(q);  // a selected candidate always occurs (c >= 2)
+        if (!pr.update(q)) {
+            set_error(sd, kErrCandOverflow, pr.m);
+            return;
+        }
+        ++n_own;
         if (tid == 0 && n_rec < sd.sub_cap)
             rec[n_rec] = q;
         ++n_rec;
