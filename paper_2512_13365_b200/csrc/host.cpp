@@ -259,6 +259,7 @@ struct DevSys {
     int W = 1;         // mask words the kernel is instantiated with
     int nt = 64;       // block size (threads per process)
     bool dense = true; // Greedy-Intersections form
+    bool bm = false;   // dense layout with per-variable candidate bitmaps
     DBuf masks, keys, cnts;
     int base_m = 0;
     int mcap_full = 0;  // > 0: h.mcap was shrunk to the starting list + slack
@@ -317,15 +318,43 @@ void choose_launch(const tcse_ctx* ctx, DevSys* d) {
 // gi form on the actual starting list (lists only shrink): the dense
 // reference loop up to 512 candidates, the O(deg) walk beyond (sweep on every
 // fixture)
+void pick_bm(DevSys* d);
+
 void pick_form(DevSys* d) {
     static const int dense_max = env_int("TCSE_GI_DENSE_MAX", 512);
     if (env_int("TCSE_GI_DENSE", -1) < 0)
         d->dense = d->base_m <= dense_max;
+    pick_bm(d);
 }
 
 int smem_one(const DevSys& d) {
     Lay L;
-    return int(carve(&L, d.W, d.nt, d.h.vcap, d.h.mcap, d.h.n_e, coin_words_for(d.h), d.dense));
+    return int(carve(&L, d.W, d.nt, d.h.vcap, d.h.mcap, d.h.n_e, coin_words_for(d.h), d.dense, d.bm));
+}
+
+// processes per SM the register cap allows (search.cu MinBlocks)
+int reg_blocks(int nt) { return nt == 32 ? 28 : (nt == 64 ? 14 : (nt == 128 ? 8 : 4)); }
+
+// Per-variable candidate bitmaps (O(m/32 + deg) pruned gi scoring) whenever
+// the dense layout prunes and the bitmaps ((V+1) * ceil(mcap/32) words more
+// shared memory per process) cost at most a quarter of the resident processes.
+// TCSE_GI_BM=0/1 forces (results never depend on it).
+void pick_bm(DevSys* d) {
+    d->bm = false;
+    if (!d->dense)
+        return;
+    const int forced = env_int("TCSE_GI_BM", -1);
+    if (forced >= 0) {
+        d->bm = forced != 0;
+        return;
+    }
+    if (env_int("TCSE_GI_PRUNE", d->base_m > 32 ? 1 : 0) == 0)
+        return;
+    const int s0 = smem_one(*d);
+    d->bm = true;
+    const int s1 = smem_one(*d);
+    const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + 1024)); };
+    d->bm = 4 * per_sm(s1) >= 3 * per_sm(s0);  // at most a quarter fewer resident processes
 }
 
 // extra_vars: fresh variables a caller-supplied prefix may add beyond the
@@ -398,6 +427,7 @@ SysDesc base_desc(const DevSys& d, int32_t* err) {
     sd.words = d.h.w_need;
     sd.coin_words = coin_words_for(d.h);
     sd.gi_dense = d.dense ? 1 : 0;
+    sd.gi_bm = d.bm ? 1 : 0;
     // near-best pruning pays once candidate lists are long enough that the
     // O(m^2) scoring outweighs its extra reductions and tie folds: on for
     // systems starting above 32 candidates (laderman-size systems, with

@@ -40,6 +40,7 @@ struct SysDesc {
     int32_t words;    // ceil(n_e / 64): words a mask needs (the launch may use more)
     int32_t coin_words;  // gi coin buffer (u32 words) per block
     int32_t gi_dense;    // 1: gi by the reference's O(m) loop per candidate; 0: O(deg) walk
+    int32_t gi_bm;       // dense: per-variable candidate bitmaps in the layout (O(m/32 + deg) scoring)
     int32_t gi_prune;    // > 0: near-best pruning (walk: exact folds only near the best; dense: from gi_prune candidates on); 0: off
     int32_t vcap;     // variable capacity = n_x + naive
     int32_t mcap;     // candidate capacity (<= pair occurrences / 2)
@@ -172,7 +173,7 @@ struct XchgLaunch {
 struct Lay {
     u32 mask, keys0, keys1, cnts0, cnts1;
     u32 tcnt, ncp, ncn, aux, newexcl;                               // update view
-    u32 qbase, wp, nA, nB, aoff, bs, cursor, alist, wbt, coin;      // gi view
+    u32 qbase, wp, nA, nB, aoff, bs, cursor, alist, wbt, coin, bm;  // gi view
     u32 mt, red, reds, redi, bcast;
     u32 coin_cap;  // coin bits of the gi view
     u32 total;     // bytes
@@ -181,7 +182,7 @@ struct Lay {
 __host__ __device__ inline u32 al16(u32 x) { return (x + 15u) & ~15u; }
 
 __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, int n_e, int coin_words,
-                                      int gi_dense) {
+                                      int gi_dense, int gi_bm) {
     const u32 NW = u32(nt / 32);
     const u32 vc = u32(vcap), mc = u32(mcap);
     u32 o = 0;
@@ -225,9 +226,14 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
         o += al16((vc + 1u) * 4u);
         L->alist = o;
         o += al16(mc * 2u);
-    } else {  // dense view: prefix sums for the exact folds of near-best candidates
+        L->bm = L->nA;
+    } else {  // dense view: prefix sums for the exact folds of near-best candidates,
+              // per-variable candidate bitmaps (bit s of row v: candidate s holds v)
         L->wp = o;
         o += al16((mc + 1u) * 4u);
+        L->bm = o;
+        if (gi_bm)
+            o += al16((vc + 1u) * ((mc + 31u) / 32u) * 4u);
         L->nB = L->aoff = L->bs = L->cursor = L->alist = L->nA;
     }
     L->wbt = o;

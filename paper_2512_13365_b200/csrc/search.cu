@@ -985,11 +985,19 @@ struct St {
         double* wbt = sp<double>(lay.wbt);
         const u32* coin = sp<u32>(lay.coin);
         // @region gi_zero
+        const int nwl = (mcap + 31) >> 5;  // bitmap row stride (words)
+        const int nwm = (m + 31) >> 5;     // words in use this step
+        u32* bm = sp<u32>(lay.bm);
 #pragma unroll 1
         for (int v = tid; v < V1; v += NT) {
             nA[v] = 0u;
             if (walk)
                 nB[v] = 0u;
+        }
+        if (approx && gi_bm) {
+#pragma unroll 1
+            for (int t = tid; t < V1 * nwm; t += NT)
+                bm[(t / nwm) * nwl + t % nwm] = 0u;
         }
 #pragma unroll 1
         for (int cc = tid; cc <= sd_ne; cc += NT)
@@ -1010,6 +1018,10 @@ struct St {
                 atomicAdd(&nA[key_i(kk)], 1u);
                 atomicAdd(&nA[key_j(kk)], 1u);
                 lmax = max(lmax, u32(c[t]) - 1u);
+                if (approx && gi_bm) {
+                    atomicOr(&bm[key_i(kk) * nwl + (t >> 5)], 1u << (t & 31));
+                    atomicOr(&bm[key_j(kk) * nwl + (t >> 5)], 1u << (t & 31));
+                }
             }
             if (approx) {
                 lmax = __reduce_max_sync(FULLMASK, lmax);
@@ -1265,13 +1277,19 @@ struct St {
                     double lb = -INFINITY, h1 = 0.0, h2 = 0.0;
                     int q1 = -1, q2 = -1;
                     bool ovf = false;
-                    for (int qb = q_lo; qb < q_hi;) {
-                        if (q_hi - qb > NT) {
-                            gi_pass<2>(qb + tid, q_hi, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
-                            qb += 2 * NT;
-                        } else {
-                            gi_pass<1>(qb + tid, q_hi, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
-                            qb += NT;
+                    if (gi_bm) {
+#pragma unroll 1
+                        for (int q = q_lo + tid; q < q_hi; q += NT)
+                            gi_score_bm(q, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+                    } else {
+                        for (int qb = q_lo; qb < q_hi;) {
+                            if (q_hi - qb > NT) {
+                                gi_pass<2>(qb + tid, q_hi, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+                                qb += 2 * NT;
+                            } else {
+                                gi_pass<1>(qb + tid, q_hi, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+                                qb += NT;
+                            }
                         }
                     }
                     B = fmax(B, block_max_d(lb));
@@ -1379,6 +1397,62 @@ struct St {
         if (q_hi - q_lo <= NT)
             return gi_dense_chunk_k<1>(ks, c, m_, q_lo, q_hi, c0, alpha, best_s, best_q);
         return gi_dense_chunk_k<3>(ks, c, m_, q_lo, q_hi, c0, alpha, best_s, best_q);
+    }
+
+    // Approximate gi score of candidate q from the per-variable candidate
+    // bitmaps: q's intersecting candidates in canonical order are the set bits
+    // of bm[qi] | bm[qj] minus q itself, so the pass is O(m/32 + deg q) instead
+    // of O(m); the k-th of them takes coin k (64-bit window: at most 64 coins
+    // per candidate on this path).  Exact integer sums packed I << 16 | C, as
+    // in gi_pass; near-best bookkeeping as in the walk's approximate pass.
+    __device__ __forceinline__ void gi_score_bm(int q, u32 c0, u32 T, double alpha, double beta, double eps2,
+                                                double& lb, int& q1, double& h1, int& q2, double& h2, bool& ovf) {
+        const u32* ks = keys();
+        const u16* c = cnts();
+        const u32* coin = sp<u32>(lay.coin);
+        const u32 kq = ks[q];
+        const int nwl = (mcap + 31) >> 5;
+        const u32* bi = sp<u32>(lay.bm) + key_i(kq) * nwl;
+        const u32* bj = sp<u32>(lay.bm) + key_j(kq) * nwl;
+        const u32 p = sp<u32>(lay.qbase)[q] - c0;
+        const u32 w0 = coin[p >> 5], w1 = coin[(p >> 5) + 1], w2 = coin[(p >> 5) + 2];
+        u32 lo = __funnelshift_r(w0, w1, p & 31u), hi = __funnelshift_r(w1, w2, p & 31u);
+        u32 A = 0u;
+        const int nwm = (m + 31) >> 5;
+#pragma unroll 1
+        for (int wd = 0; wd < nwm; ++wd) {
+            u32 msk = bi[wd] | bj[wd];
+            if (wd == (q >> 5))
+                msk &= ~(1u << (q & 31));
+            while (msk) {
+                const int s = (wd << 5) + __ffs(msk) - 1;
+                msk &= msk - 1;
+                const u32 w = u32(c[s]) - 1u;
+                A += (w << 16) + ((lo & 1u) ? w : 0u);
+                lo = __funnelshift_r(lo, hi, 1);
+                hi >>= 1;
+            }
+        }
+        const u32 wq = u32(c[q]) - 1u;
+        const double F = __dadd_rn(double(T - wq - (A >> 16)), __dmul_rn(beta, double(A & 0xffffu)));
+        const double h = __dadd_rn(double(wq), __dmul_rn(alpha, F));
+        lb = fmax(lb, h);
+        const double lim = __dsub_rn(lb, eps2);
+        if (q1 >= 0 && h1 < lim)
+            q1 = -1;
+        if (q2 >= 0 && h2 < lim)
+            q2 = -1;
+        if (h >= lim) {
+            if (q1 < 0) {
+                q1 = q;
+                h1 = h;
+            } else if (q2 < 0) {
+                q2 = q;
+                h2 = h;
+            } else {
+                ovf = true;
+            }
+        }
     }
 
     // Approximate gi scores of candidates q0, q0 + NT, ..., q0 + (K-1) NT
@@ -1716,6 +1790,7 @@ struct St {
     }
 
     int sd_ne;
+    int gi_bm;     // dense layout carries per-variable candidate bitmaps
     int gi_prune;  // 0: no pruning (test hook); dense layout: prune from this many candidates on
     int mcap;  // candidate capacity of the layout
 };
@@ -1767,7 +1842,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     // ---- process configuration (prep_kernel) + base state (all threads)
     __shared__ SlotRec s_slot;
     if (tid == 0) {
-        carve(&lay, W, NT, sd.vcap, sd.mcap, sd.n_e, sd.coin_words, sd.gi_dense);
+        carve(&lay, W, NT, sd.vcap, sd.mcap, sd.n_e, sd.coin_words, sd.gi_dense, sd.gi_bm);
         s_slot = L.slots[blk];
     }
     __syncthreads();
@@ -1816,6 +1891,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     pr.last_coins = 0;
     pr.sd_ne = sd.n_e;
     pr.gi_prune = sd.gi_prune;
+    pr.gi_bm = sd.gi_bm;
     pr.mcap = sd.mcap;
     if (sd.base_keys) {
         pr.m = sd.base_m;

@@ -2,7 +2,8 @@
 sel_gi / add_run): the dense layout (TCSE_GI_DENSE=1) and the O(deg) walk
 (TCSE_GI_DENSE=0), forced on the same processes — each both with near-best
 pruning (default: approximate scores from exact integer sums, exact folds only
-within the rounding bound of the best; dense: gi_pass + gi_fold_dense) and
+within the rounding bound of the best; dense: gi_score_bm or gi_pass, then
+gi_fold_dense) and
 without it (TCSE_GI_PRUNE=0: the walk folds every candidate, the dense layout
 runs the reference loop itself).
 
@@ -66,10 +67,13 @@ def systems(rng):
     return out
 
 
-@pytest.mark.parametrize("form", ["1", "1-exact", "0", "0-exact"])
+@pytest.mark.parametrize("form", ["1", "1-nobm", "1-exact", "0", "0-exact"])
 def test_gi_forms_match_oracle(dev, monkeypatch, form):
     monkeypatch.setenv("TCSE_GI_DENSE", form[0])
     monkeypatch.setenv("TCSE_GI_PRUNE", "0" if form.endswith("exact") else "1")
+    # dense pruned scoring: per-variable candidate bitmaps (gi_score_bm) or the
+    # full-list pass (gi_pass)
+    monkeypatch.setenv("TCSE_GI_BM", "0" if form.endswith("nobm") else "1")
     rng = random.Random(4242)
     for sys_ in systems(rng):
         cfgs = gi_cfgs(rng, 18)
