@@ -996,8 +996,10 @@ struct St {
         }
         if (approx && gi_bm) {
 #pragma unroll 1
-            for (int t = tid; t < V1 * nwm; t += NT)
-                bm[(t / nwm) * nwl + t % nwm] = 0u;
+            for (int v = tid; v < V1; v += NT)
+#pragma unroll 1
+                for (int w = 0; w < nwm; ++w)
+                    bm[v * nwl + w] = 0u;
         }
 #pragma unroll 1
         for (int cc = tid; cc <= sd_ne; cc += NT)
