@@ -1949,6 +1949,8 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             }
         }
     }
+    const int sub_cap = sd.sub_cap;
+    const u64 we = u64(sd.words);
     while (!dump) {
         if (trace && tid == 0 && step < sd.trace_stride)
             trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
@@ -1962,7 +1964,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             strat = uniform_real(pr.draw(), 0.0, 1.0) < p_greedy ? TCSE_GREEDY_ALTERNATIVE : TCSE_WEIGHTED_RANDOM;
         if ((strat == TCSE_GREEDY_INTERSECTIONS || strat == TCSE_GREEDY_POTENTIAL) && alpha == 0.0)
             strat = TCSE_GREEDY;  // gain only (strategies.hpp:140-141, 205-206)
-        const u64 Vt = u64(pr.V), mt_ = u64(pr.m), we = u64(sd.words);
+        const u64 Vt = u64(pr.V), mt_ = u64(pr.m);
         int pick;
         u64 sel = mt_;
         if (strat == TCSE_GREEDY) {
@@ -1987,13 +1989,13 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             return;
         }
         ++n_own;
-        if (tid == 0 && n_rec < sd.sub_cap)
-            rec[n_rec] = q;
-        ++n_rec;
-        if (n_rec > sd.sub_cap) {
-            set_error(sd, TCSE_ECAPACITY, n_rec);
+        if (n_rec >= sub_cap) {  // the record would outgrow its row
+            set_error(sd, TCSE_ECAPACITY, n_rec + 1);
             return;
         }
+        if (tid == 0)
+            rec[n_rec] = q;
+        ++n_rec;
     }
 
     if (dump) {
