@@ -1922,7 +1922,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     u32* rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
     u64* trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
     const bool dump = sd.mode == kModeDump;
-    int n_rec = 0, n_own = 0, step = 0;
+    int n_rec = 0, step = 0;
     u64 wops = 0;
     // prefix replay (reinit from the incumbent, or a fixed replay): apply +
     // update only, its own loop so the search loop carries no prefix state
@@ -1949,12 +1949,15 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             }
         }
     }
+    const int n_rec0 = n_rec;  // steps selected by this process = n_rec - n_rec0
     const int sub_cap = sd.sub_cap;
     const u64 we = u64(sd.words);
     while (!dump) {
-        if (trace && tid == 0 && step < sd.trace_stride)
-            trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
-        ++step;
+        if (trace) {  // parity hook only
+            if (tid == 0 && step < sd.trace_stride)
+                trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
+            ++step;
+        }
         if (pr.m == 0)
             break;
         int strat = strategy;
@@ -1988,7 +1991,6 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             set_error(sd, kErrCandOverflow, pr.m);
             return;
         }
-        ++n_own;
         if (n_rec >= sub_cap) {  // the record would outgrow its row
             set_error(sd, TCSE_ECAPACITY, n_rec + 1);
             return;
@@ -2019,7 +2021,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     if (tid == 0) {
         sd.out_cost[lp] = pr.cost;
         sd.out_len[lp] = n_rec;
-        sd.out_own[lp] = n_own;
+        sd.out_own[lp] = n_rec - n_rec0;
         sd.out_strategy[lp] = strategy;
         sd.out_seed[lp] = s_slot.seed;
         if (sd.out_wops)
