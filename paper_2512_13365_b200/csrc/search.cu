@@ -798,60 +798,49 @@ struct St {
             m = int(sc >> 32);
             return true;
         }
-        // (c) one packed scan: low 16 bits old survivors, high 16 bits new pairs
-        const int L = m + 2 * (k - 1);
-        const int E = (L + NT - 1) / NT;
-        const int e0 = min(L, tid * E), e1 = min(L, e0 + E);
-        u32 local = 0;
+        // (c) general case: old survivors of this thread's candidate range
+        // [a0, a1) (counted in (a)) and new pairs (x, k, +/-) of its variable
+        // range [x0, x1) within [1, k); one packed scan, low 16 bits old
+        const int Ex = (k - 1 + NT - 1) / NT;
+        const int x0 = min(k, 1 + tid * Ex), x1 = min(k, x0 + Ex);
+        u32 nn = 0;
 #pragma unroll 1
-        for (int e = e0; e < e1; ++e) {
-            if (e < m) {
-                local += tcnt[e] >= 2 ? 1u : 0u;
-            } else {
-                const int x = ((e - m) >> 1) + 1;
-                const u16 c = ((e - m) & 1) ? ncn[x] : ncp[x];
-                local += c >= 2 ? 0x10000u : 0u;
-            }
-        }
-        u32 total;
-        const u64 sc_excl = block_scan_ool<NT>(local, red());
-        u32 excl = u32(sc_excl);
-        total = u32(sc_excl >> 32);
+        for (int x = x0; x < x1; ++x)
+            nn += (ncp[x] >= 2 ? 1u : 0u) + (ncn[x] >= 2 ? 1u : 0u);
+        const u64 sc_excl = block_scan_ool<NT>(keep | (nn << 16), red());
+        const u32 excl = u32(sc_excl), total = u32(sc_excl >> 32);
         const u32 n_old = total & 0xffffu, n_new = total >> 16;
         if (int(n_old + n_new) > mcap)
             return false;
         u32 o = excl & 0xffffu, n = excl >> 16;
 #pragma unroll 1
-        for (int e = e0; e < e1; ++e) {
-            if (e < m) {
-                aux[e] = o;
-                o += tcnt[e] >= 2 ? 1u : 0u;
-            } else {
-                const int x = ((e - m) >> 1) + 1;
-                const int sg = (e - m) & 1;
-                if (!sg)
-                    newexcl[x] = n;
-                n += ((sg ? ncn[x] : ncp[x]) >= 2) ? 1u : 0u;
-            }
+        for (int t = a0; t < a1; ++t) {
+            aux[t] = o;
+            o += tcnt[t] >= 2 ? 1u : 0u;
+        }
+#pragma unroll 1
+        for (int x = x0; x < x1; ++x) {
+            newexcl[x] = n;
+            n += (ncp[x] >= 2 ? 1u : 0u) + (ncn[x] >= 2 ? 1u : 0u);
         }
         __syncthreads();
         u32* dk = sp<u32>(cur ? lay.keys0 : lay.keys1);
         u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
         o = excl & 0xffffu;
+#pragma unroll 1
+        for (int t = a0; t < a1; ++t)
+            if (tcnt[t] >= 2) {
+                const u32 kk = ok[t];
+                const u32 dest = o + newexcl[key_i(kk)];
+                dk[dest] = kk;
+                dc[dest] = tcnt[t];
+                ++o;
+            }
         n = excl >> 16;
 #pragma unroll 1
-        for (int e = e0; e < e1; ++e) {
-            if (e < m) {
-                if (tcnt[e] >= 2) {
-                    const u32 kk = ok[e];
-                    const u32 dest = o + newexcl[key_i(kk)];
-                    dk[dest] = kk;
-                    dc[dest] = tcnt[e];
-                    ++o;
-                }
-            } else {
-                const int x = ((e - m) >> 1) + 1;
-                const int sg = (e - m) & 1;
+        for (int x = x0; x < x1; ++x) {
+#pragma unroll 1
+            for (int sg = 0; sg < 2; ++sg) {
                 const u16 c = sg ? ncn[x] : ncp[x];
                 if (c >= 2) {
                     // old survivors before (x, k, .) are those with i <= x
