@@ -1086,14 +1086,23 @@ struct St {
                 if (lane == 0)
                     atomicMax(s_dmax, dmax);
             }
-            const u64 sc_exd = block_scan_ool<NT>(ld, red());
-            u32 exd = u32(sc_exd);
-            D = u32(sc_exd >> 32);
-            u32 W_ = 0, exw = 0;
-            if (walk || approx) {
-                const u64 sc_w = block_scan_ool<NT>(lw, red());
-                exw = u32(sc_w);
-                W_ = u32(sc_w >> 32);
+            u32 exd, W_ = 0, exw = 0;
+            if ((walk || approx) && m <= 180 && u32(m) * (*s_wmax + 1u) < 65536u) {
+                // degrees (sum <= 2 m^2) and weights in one packed 16/16 scan
+                const u64 sc = block_scan_ool<NT>(ld | (lw << 16), red());
+                exd = u32(sc) & 0xffffu;
+                exw = u32(sc) >> 16;
+                D = u32(sc >> 32) & 0xffffu;
+                W_ = u32(sc >> 32) >> 16;
+            } else {
+                const u64 sc_exd = block_scan_ool<NT>(ld, red());
+                exd = u32(sc_exd);
+                D = u32(sc_exd >> 32);
+                if (walk || approx) {
+                    const u64 sc_w = block_scan_ool<NT>(lw, red());
+                    exw = u32(sc_w);
+                    W_ = u32(sc_w >> 32);
+                }
             }
             u32* wp = sp<u32>(lay.wp);
 #pragma unroll 1
