@@ -113,7 +113,7 @@ struct LaunchDesc {
     SlotRec* slots;  // [total_blocks]
     u64* rng;        // [total_blocks][312] seeded mt19937_64 states
     int32_t* perm;   // [total_blocks] launch order -> block (grouped by strategy), or null
-    int32_t* hist;   // [kMaxSys][16] strategy histogram + placement cursors
+    int32_t* hist;   // [kMaxSys][32] (strategy, fresh/reinit) histogram + placement cursors
     const SysDesc* table;  // > kMaxSys systems (flip mode): device table, blocks contiguous per system
     int32_t table_n;
     SysDesc sys[kMaxSys];

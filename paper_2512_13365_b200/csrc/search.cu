@@ -2083,8 +2083,8 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     r.p_greedy = sl.p_greedy;
     r.seed = sl.seed;
     L.slots[b] = r;
-    if (L.hist)
-        atomicAdd(&L.hist[s * 16 + st], 1);
+    if (L.hist)  // buckets (strategy, fresh / reinit)
+        atomicAdd(&L.hist[s * 32 + st + 8 * reinit], 1);
     if (rng) {
         // optimize_with_flips seeds each (process, component) stream from
         // mix_seed{slot.seed, comp} (parallel_search.hpp:441)
@@ -2113,11 +2113,15 @@ __global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ Laun
         return;
     const int order[7] = {TCSE_GREEDY_POTENTIAL, TCSE_GREEDY_INTERSECTIONS, TCSE_MIXED, TCSE_GREEDY_RANDOM,
                           TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY};
-    const int st = L.slots[b].strategy;
+    // within a strategy, fresh processes before reinit ones (which replay part
+    // of the incumbent instead of selecting: shorter)
+    const int st = L.slots[b].strategy, ri = L.slots[b].reinit ? 1 : 0;
     int base = sd.block_begin;
     for (int k = 0; k < 7 && order[k] != st; ++k)
-        base += L.hist[s * 16 + order[k]];
-    L.perm[base + atomicAdd(&L.hist[s * 16 + 8 + st], 1)] = b;
+        base += L.hist[s * 32 + order[k]] + L.hist[s * 32 + 8 + order[k]];
+    if (ri)
+        base += L.hist[s * 32 + st];
+    L.perm[base + atomicAdd(&L.hist[s * 32 + 16 + st + 8 * ri], 1)] = b;
 }
 
 // ----------------------------------------------------------------- K2
@@ -2355,7 +2359,7 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int 
 cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
     const int g = (L.total_blocks + 127) / 128;
     if (L.hist) {
-        cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * 16 * kMaxSys, st);
+        cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * 32 * kMaxSys, st);
         if (e != cudaSuccess)
             return e;
     }
