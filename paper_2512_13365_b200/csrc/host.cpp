@@ -384,7 +384,7 @@ int reserve_prep(tcse_ctx* ctx, int blocks) {
     CU(ctx->slots.reserve(b * sizeof(SlotRec)));
     CU(ctx->rng.reserve(b * 312 * 8));
     CU(ctx->perm.reserve(b * 4));
-    CU(ctx->hist.reserve(sizeof(int32_t) * 32 * kMaxSys * (kMaxSys + 1)));
+    CU(ctx->hist.reserve(sizeof(int32_t) * kHistStride * kMaxSys * (kMaxSys + 1)));
     return TCSE_OK;
 }
 
@@ -400,7 +400,7 @@ int attach_prep(tcse_ctx* ctx, LaunchDesc* L, int block_offset = 0, int group = 
     static const int order = env_int("TCSE_ORDER", 1);
     if (order && L->sys[0].mode == kModeSearch) {
         L->perm = ctx->perm.as<int32_t>() + block_offset;
-        L->hist = ctx->hist.as<int32_t>() + 32 * kMaxSys * group;  // one per concurrent launch group
+        L->hist = ctx->hist.as<int32_t>() + kHistStride * kMaxSys * group;  // one per concurrent launch group
     }
     return TCSE_OK;
 }

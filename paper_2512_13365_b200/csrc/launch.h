@@ -19,6 +19,10 @@ typedef uint8_t u8;
 
 constexpr int kMaxSys = 4;
 constexpr int kCoinWords = 512;  // 16384 coin bits per gi scoring chunk
+// placement histogram per system: (strategy, work class) counts, then cursors;
+// class 0 = fresh processes, 1..4 = reinit ones by replayed-prefix quartile
+constexpr int kWorkClasses = 5;
+constexpr int kHistStride = 2 * 8 * kWorkClasses;
 
 // pair key: canonical order == unsigned key order (linear_system.hpp:32-36)
 //   bits 31..17: i (1-based, < 2^15), 16..1: j (< 2^16), 0: rel_sign < 0
@@ -113,7 +117,7 @@ struct LaunchDesc {
     SlotRec* slots;  // [total_blocks]
     u64* rng;        // [total_blocks][312] seeded mt19937_64 states
     int32_t* perm;   // [total_blocks] launch order -> block (grouped by strategy), or null
-    int32_t* hist;   // [kMaxSys][32] (strategy, fresh/reinit) histogram + placement cursors
+    int32_t* hist;   // [kMaxSys][kHistStride] (strategy, work class) histogram + placement cursors
     const SysDesc* table;  // > kMaxSys systems (flip mode): device table, blocks contiguous per system
     int32_t table_n;
     SysDesc sys[kMaxSys];

@@ -2083,8 +2083,6 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     r.p_greedy = sl.p_greedy;
     r.seed = sl.seed;
     L.slots[b] = r;
-    if (L.hist)  // buckets (strategy, fresh / reinit)
-        atomicAdd(&L.hist[s * 32 + st + 8 * reinit], 1);
     if (rng) {
         // optimize_with_flips seeds each (process, component) stream from
         // mix_seed{slot.seed, comp} (parallel_search.hpp:441)
@@ -2094,6 +2092,21 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
             ps = splitmix64(ps ^ u64(sd.stream_comp));
         }
         mt_seed(L.rng + size_t(b) * 312, ps);
+    }
+    if (L.hist) {
+        // placement bucket (strategy, work class): fresh processes, then reinit
+        // ones by the length of their replayed prefix (estimated from the
+        // first output of their stream, ignoring the rare rejection: the
+        // order never changes results)
+        int cls = 0;
+        if (reinit) {
+            const u64* m0 = L.rng + size_t(b) * 312;
+            const u64 x = mt_temper(mt_mix(m0[0], m0[1], m0[156]));
+            const u64 n_pre = 1 + __umul64hi(x, u64(3 * sd.inc_len / 4));
+            cls = 1 + min(3, int(4 * n_pre / u64(sd.inc_len + 1)));
+        }
+        L.slots[b].pad = cls;
+        atomicAdd(&L.hist[s * kHistStride + st + 8 * cls], 1);
     }
 }
 
@@ -2115,13 +2128,16 @@ __global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ Laun
                           TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY};
     // within a strategy, fresh processes before reinit ones (which replay part
     // of the incumbent instead of selecting: shorter)
-    const int st = L.slots[b].strategy, ri = L.slots[b].reinit ? 1 : 0;
+    const int st = L.slots[b].strategy, cls = L.slots[b].pad;
+    const int* h = L.hist + s * kHistStride;
     int base = sd.block_begin;
     for (int k = 0; k < 7 && order[k] != st; ++k)
-        base += L.hist[s * 32 + order[k]] + L.hist[s * 32 + 8 + order[k]];
-    if (ri)
-        base += L.hist[s * 32 + st];
-    L.perm[base + atomicAdd(&L.hist[s * 32 + 16 + st + 8 * ri], 1)] = b;
+#pragma unroll
+        for (int c = 0; c < kWorkClasses; ++c)
+            base += h[order[k] + 8 * c];
+    for (int c = 0; c < cls; ++c)
+        base += h[st + 8 * c];
+    L.perm[base + atomicAdd(&L.hist[s * kHistStride + 8 * kWorkClasses + st + 8 * cls], 1)] = b;
 }
 
 // ----------------------------------------------------------------- K2
@@ -2359,7 +2375,7 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int 
 cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
     const int g = (L.total_blocks + 127) / 128;
     if (L.hist) {
-        cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * 32 * kMaxSys, st);
+        cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * kHistStride * kMaxSys, st);
         if (e != cudaSuccess)
             return e;
     }
