@@ -649,13 +649,16 @@ struct St {
     }
 
     // n coin flips (uniform_int_distribution<int>(0,1) == top tempered bit)
-    __device__ void draw_coins(u32 nbits) {
+    // precleared: the caller zeroed the buffer's first words behind a barrier
+    __device__ void draw_coins(u32 nbits, bool precleared = false) {
         u32* coin = sp<u32>(lay.coin);
-        const u32 words = (nbits + 31) >> 5;
+        if (!precleared) {
+            const u32 words = (nbits + 31) >> 5;
 #pragma unroll 1
-        for (u32 w = tid; w < words; w += NT)
-            coin[w] = 0u;
-        __syncthreads();
+            for (u32 w = tid; w < words; w += NT)
+                coin[w] = 0u;
+            __syncthreads();
+        }
         u32 done = 0;
         while (done < nbits) {
             if (mti >= 312) {
@@ -1120,6 +1123,13 @@ struct St {
                 if (walk || approx)
                     wp[m] = W_;
             }
+            if (dense) {  // the first coin chunk's words, behind the barrier below
+                u32* coin = sp<u32>(lay.coin);
+                const u32 words = (min(D, lay.coin_cap) + 31) >> 5;
+#pragma unroll 1
+                for (u32 w = tid; w < words; w += NT)
+                    coin[w] = 0u;
+            }
         }
         __syncthreads();
         last_coins = D;
@@ -1267,7 +1277,7 @@ struct St {
                         hi = mid - 1;
                 }
                 const int q_hi = lo;
-                draw_coins(qbase[q_hi] - c0);
+                draw_coins(qbase[q_hi] - c0, dense && q_lo == 0);  // walk layout (beta < 0) clears here
                 if (!use_approx) {
                     GI_STAT(4, 1);
                     const double2 r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
@@ -1330,7 +1340,8 @@ struct St {
                         }
                     }
                 }
-                __syncthreads();
+                if (q_hi < m)  // the coin buffer is refilled; after the last chunk argmax's barrier suffices
+                    __syncthreads();
                 q_lo = q_hi;
             }
         }
