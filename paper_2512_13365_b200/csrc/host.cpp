@@ -271,7 +271,8 @@ int coin_words_for(const HostSys& h) {
     // gi coin bits: all coins of a step fit for typical states (sum of
     // degrees), else the kernel evaluates gi densely in chunks
     const long long want = (long long)h.mcap * 24 / 32 + 64;
-    return int(std::min<long long>(std::max<long long>(want, 256), 2048));
+    static const int floor_words = env_int("TCSE_COIN_MIN", 64);
+    return int(std::min<long long>(std::max<long long>(want, floor_words), 2048));
 }
 
 // gi evaluation form: the O(deg) walk pays off once candidate lists are long
