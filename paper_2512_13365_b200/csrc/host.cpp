@@ -272,7 +272,10 @@ int coin_words_for(const HostSys& h) {
     // degrees), else the kernel evaluates gi densely in chunks
     const long long want = (long long)h.mcap * 24 / 32 + 64;
     static const int floor_words = env_int("TCSE_COIN_MIN", 64);
-    return int(std::min<long long>(std::max<long long>(want, floor_words), 2048));
+    // TCSE_COIN_MAX (test hook): a small buffer forces many coin chunks per step
+    // (never below one candidate's coins: deg q <= 2 (mcap - 1))
+    const int cap_words = std::max((2 * h.mcap + 31) / 32 + 1, std::min(env_int("TCSE_COIN_MAX", 2048), 2048));
+    return int(std::min<long long>(std::max<long long>(want, std::min(floor_words, cap_words)), cap_words));
 }
 
 // gi evaluation form: the O(deg) walk pays off once candidate lists are long

@@ -103,3 +103,22 @@ def test_negative_scores_gp(dev):
         cfgs = [T.ProcessConfig(6, alpha=rng.choice([-0.5, -2.0, -7.5]), seed=rng.getrandbits(64)) for _ in range(8)]
         for cfg, rec in zip(cfgs, T.run_cse(sys_, cfgs)):
             assert (rec.substitutions, rec.cost) == o_run_cse(sys_, cfg), cfg
+
+
+@pytest.mark.parametrize("form", ["1", "1-nobm", "1-exact", "0"])
+def test_gi_forms_many_coin_chunks(dev, monkeypatch, form):
+    """A coin buffer of one candidate's worth (TCSE_COIN_MAX) splits every gi
+    step into many chunks: chunk boundaries, the precleared first chunk and the
+    per-chunk near-best folds must still reproduce the oracle."""
+    monkeypatch.setenv("TCSE_COIN_MAX", "1")
+    monkeypatch.setenv("TCSE_GI_DENSE", form[0])
+    monkeypatch.setenv("TCSE_GI_PRUNE", "0" if form.endswith("exact") else "1")
+    monkeypatch.setenv("TCSE_GI_BM", "0" if form.endswith("nobm") else "1")
+    rng = random.Random(777)
+    for sys_ in systems(rng)[:8]:
+        cfgs = gi_cfgs(rng, 12)
+        recs, traces = T.run_cse(sys_, cfgs, trace_stride=32)
+        for cfg, rec, tr in zip(cfgs, recs, traces):
+            subs, cost, otr = o_run_cse(sys_, cfg, trace_cap=32)
+            assert (rec.substitutions, rec.cost) == (subs, cost), (form, cfg)
+            assert tr == otr, (form, cfg)
