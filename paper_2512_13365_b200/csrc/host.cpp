@@ -270,7 +270,7 @@ namespace {
 int coin_words_for(const HostSys& h) {
     // gi coin bits: all coins of a step fit for typical states (sum of
     // degrees), else the kernel evaluates gi densely in chunks
-    const long long want = (long long)h.mcap * 24 / 32 + 64;
+    const long long want = (long long)h.mcap * 24 / 32 + 8;
     static const int floor_words = env_int("TCSE_COIN_MIN", 64);
     // TCSE_COIN_MAX (test hook): a small buffer forces many coin chunks per step
     // (never below one candidate's coins: deg q <= 2 (mcap - 1))

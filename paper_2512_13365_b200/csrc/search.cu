@@ -1302,12 +1302,9 @@ struct St {
                             }
                         }
                     }
-                    B = fmax(B, block_max_d(lb));
+                    const u32 info = near_best(lb, eps2, q1, h1, q2, h2, ovf, B);
                     const double thr = __dsub_rn(B, eps2);
                     const bool k1 = q1 >= 0 && h1 >= thr, k2 = q2 >= 0 && h2 >= thr;
-                    const u32 ns = u32(k1) + u32(k2);
-                    u32 info = (ovf ? 0x10000u : 0u) + ns;
-                    info = block_sum<NT>(info, red());
                     GI_STAT(0, 1);
                     GI_STAT(5, m);
                     if (info >> 16) {
@@ -1603,6 +1600,52 @@ struct St {
         for (int w = 1; w < NW; ++w)
             b = fmax(b, r[w]);
         return b;
+    }
+
+    // Dense gi pruning in one barrier: B = max(B, block max of lb) and the
+    // near-best count (ovf flags << 16 | candidates >= B - eps2).  Each warp
+    // publishes its max and its count relative to its own max; a warp whose
+    // max is B counts exactly, another warp within the window counts as 1
+    // (a lower bound: it holds at least its max).  So the count is exact
+    // whenever it is <= 1 on a single chunk, the only case that decides
+    // anything (the lone pick); ovf is the OR over the block as before.
+    __device__ __forceinline__ u32 near_best(double lb, double eps2, int q1, double h1, int q2, double h2, bool ovf,
+                                             double& B) {
+        double wm = lb;
+        wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 16));
+        wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 8));
+        wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 4));
+        wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 2));
+        wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 1));
+        const double wthr = __dsub_rn(wm, eps2);
+        u32 wi = (ovf ? 0x10000u : 0u) + u32(q1 >= 0 && h1 >= wthr) + u32(q2 >= 0 && h2 >= wthr);
+        wi = __reduce_add_sync(FULLMASK, wi);
+        if (NW == 1) {
+            B = fmax(B, wm);
+            return wi;
+        }
+        rsel ^= 1;
+        double* r = sp<double>(lay.reds) + rsel * NW;
+        u32* ri = reinterpret_cast<u32*>(sp<int>(lay.redi) + rsel * NW);
+        if (lane == 0) {
+            r[tid >> 5] = wm;
+            ri[tid >> 5] = wi;
+        }
+        __syncthreads();
+        double cm = r[0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w)
+            cm = fmax(cm, r[w]);
+        B = fmax(B, cm);
+        const double thr = __dsub_rn(B, eps2);
+        u32 info = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const double x = r[w];
+            const u32 y = ri[w];
+            info += (y & 0xffff0000u) + (x >= thr ? (x == B ? (y & 0xffffu) : 1u) : 0u);
+        }
+        return info;
     }
 
     // Candidate q's intersecting candidates in canonical order: the merge of
