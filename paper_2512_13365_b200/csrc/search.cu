@@ -891,22 +891,16 @@ struct St {
         for (int t = tid; t < m; t += NT)
             mx = max(mx, u32(c[t]));
         mx = block_max<NT>(mx, red());
-        u32 cnt = 0;
-#pragma unroll 1
-        for (int t = tid; t < m; t += NT)
-            cnt += c[t] == mx ? 1u : 0u;
-        cnt = block_sum<NT>(cnt, red());
-        const u32 r = u32(nd(cnt));
+        // the argmax set's size is the scan's total (one pass, one barrier less)
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
         u32 local = 0;
 #pragma unroll 1
         for (int e = e0; e < e1; ++e)
             local += c[e] == mx ? 1u : 0u;
-        u32 total;
         const u64 sc_ex = block_scan_ool<NT>(local, red());
         u32 ex = u32(sc_ex);
-        total = u32(sc_ex >> 32);
+        const u32 r = u32(nd(u32(sc_ex >> 32)));
         u32* bc = sp<u32>(lay.bcast);
 #pragma unroll 1
         for (int e = e0; e < e1; ++e)
@@ -923,25 +917,19 @@ struct St {
     __device__ int sel_wr() {
         const u16* c = cnts();
         u32* bc = sp<u32>(lay.bcast);
-        u32 tot = 0;
-#pragma unroll 1
-        for (int t = tid; t < m; t += NT)
-            tot += u32(c[t]) - 1u;
-        tot = block_sum<NT>(tot, red());
-        const double target = __dmul_rn(uniform_real(draw(), 0.0, 1.0), double(tot));
+        // the total weight is the scan's total (one pass, two barriers less);
+        // bc[1] was last read before the previous substitution's barriers
         if (tid == 0)
             bc[1] = u32(m - 1);
-        __syncthreads();
         const int E = (m + NT - 1) / NT;
         const int e0 = min(m, tid * E), e1 = min(m, e0 + E);
         u32 local = 0;
 #pragma unroll 1
         for (int e = e0; e < e1; ++e)
             local += u32(c[e]) - 1u;
-        u32 total;
         const u64 sc_s = block_scan_ool<NT>(local, red());
         u32 s = u32(sc_s);
-        total = u32(sc_s >> 32);
+        const double target = __dmul_rn(uniform_real(draw(), 0.0, 1.0), double(u32(sc_s >> 32)));
 #pragma unroll 1
         for (int e = e0; e < e1; ++e) {
             const u32 s1 = s + u32(c[e]) - 1u;
