@@ -144,20 +144,19 @@ __device__ __forceinline__ u32 block_scan(u32 v, u32* red, u32* total) {
         *total = __shfl_sync(FULLMASK, inc, 31);
         return inc - v;
     }
+    // one barrier: every thread adds the (at most 8) warp totals itself
     if (lane == 31)
         red[warp] = inc;
     __syncthreads();
-    if (warp == 0) {
-        const u32 w = lane < NW ? red[lane] : 0u;
-        const u32 wi = warp_incl_scan(w, lane);
-        if (lane < NW)
-            red[lane] = wi - w;
-        if (lane == NW - 1)
-            red[NW] = wi;
+    u32 pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const u32 x = red[w];
+        tot += x;
+        pre += w < warp ? x : 0u;
     }
-    __syncthreads();
-    *total = red[NW];
-    return red[warp] + inc - v;
+    *total = tot;
+    return pre + inc - v;
 }
 
 // out of line (one copy per kernel instead of one per call site): low 32
@@ -783,12 +782,13 @@ struct St {
             ncn[x] = u16(cn);
             anynew |= (cp >= 2) | (cn >= 2);
         }
-        if (!__syncthreads_or(anynew)) {
+        // survivors' scan, high half: threads that found a repeating (x, k, .)
+        const u64 sc = block_scan_ool<NT>(keep | (anynew ? 0x10000u : 0u), red());
+        if ((sc >> 48) == 0) {
             // common case: no pair with k repeats, the list only loses entries
-            const u64 sc = block_scan_ool<NT>(keep, red());
             u32* dk = sp<u32>(cur ? lay.keys0 : lay.keys1);
             u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
-            u32 o = u32(sc);
+            u32 o = u32(sc) & 0xffffu;
 #pragma unroll 1
             for (int t = a0; t < a1; ++t)
                 if (tcnt[t] >= 2) {
@@ -798,7 +798,7 @@ struct St {
                 }
             __syncthreads();
             cur ^= 1;
-            m = int(sc >> 32);
+            m = int((sc >> 32) & 0xffffu);
             return true;
         }
         // (c) general case: old survivors of this thread's candidate range
