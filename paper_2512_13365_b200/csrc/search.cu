@@ -1290,7 +1290,8 @@ struct St {
                             }
                         }
                     }
-                    const u32 info = near_best(lb, eps2, q1, h1, q2, h2, ovf, B);
+                    int lone = 0;
+                    const u32 info = near_best(lb, eps2, q1, h1, q2, h2, ovf, B, lone);
                     const double thr = __dsub_rn(B, eps2);
                     const bool k1 = q1 >= 0 && h1 >= thr, k2 = q2 >= 0 && h2 >= thr;
                     GI_STAT(0, 1);
@@ -1302,11 +1303,9 @@ struct St {
                         best_q = __double_lo_as_int(r.y);
                     } else if ((info & 0xffffu) == 1u && q_lo == 0 && q_hi == m) {
                         // a lone near-best candidate is the reference's pick
+                        // (single chunk: no argmax pass, every thread knows it)
                         GI_STAT(1, 1);
-                        if (k1)
-                            gi_keep(h1, q1, best_s, best_q);
-                        if (k2)
-                            gi_keep(h2, q2, best_s, best_q);
+                        return lone;
                     } else {
                         // fold every near-best candidate exactly, one warp each
                         GI_STAT(6, 1);
@@ -1592,13 +1591,13 @@ struct St {
 
     // Dense gi pruning in one barrier: B = max(B, block max of lb) and the
     // near-best count (ovf flags << 16 | candidates >= B - eps2).  Each warp
-    // publishes its max and its count relative to its own max; a warp whose
-    // max is B counts exactly, another warp within the window counts as 1
-    // (a lower bound: it holds at least its max).  So the count is exact
-    // whenever it is <= 1 on a single chunk, the only case that decides
-    // anything (the lone pick); ovf is the OR over the block as before.
+    // publishes its max, its count relative to its own max and the index of
+    // its max; a warp whose max is B counts exactly, another warp within the
+    // window counts as 1 (a lower bound: it holds at least its max).  So the
+    // count is exact whenever it is <= 1 on a single chunk, the only case that
+    // decides anything: then `lone` is the pick (the candidate scoring B).
     __device__ __forceinline__ u32 near_best(double lb, double eps2, int q1, double h1, int q2, double h2, bool ovf,
-                                             double& B) {
+                                             double& B, int& lone) {
         double wm = lb;
         wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 16));
         wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 8));
@@ -1606,11 +1605,14 @@ struct St {
         wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 2));
         wm = fmax(wm, __shfl_xor_sync(FULLMASK, wm, 1));
         const double wthr = __dsub_rn(wm, eps2);
-        u32 wi = (ovf ? 0x10000u : 0u) + u32(q1 >= 0 && h1 >= wthr) + u32(q2 >= 0 && h2 >= wthr);
+        u32 wi = (ovf ? 0x1000000u : 0u) + (u32(q1 >= 0 && h1 >= wthr) + u32(q2 >= 0 && h2 >= wthr)) * 0x10000u;
         wi = __reduce_add_sync(FULLMASK, wi);
+        const u32 qm = lb != wm ? 0xffffu : (q1 >= 0 && h1 == lb ? u32(q1) : (q2 >= 0 && h2 == lb ? u32(q2) : 0xffffu));
+        wi |= __reduce_min_sync(FULLMASK, qm);
         if (NW == 1) {
             B = fmax(B, wm);
-            return wi;
+            lone = int(wi & 0xffffu);
+            return ((wi >> 24) << 16) | ((wi >> 16) & 0xffu);
         }
         rsel ^= 1;
         double* r = sp<double>(lay.reds) + rsel * NW;
@@ -1631,7 +1633,9 @@ struct St {
         for (int w = 0; w < NW; ++w) {
             const double x = r[w];
             const u32 y = ri[w];
-            info += (y & 0xffff0000u) + (x >= thr ? (x == B ? (y & 0xffffu) : 1u) : 0u);
+            info += ((y >> 24) << 16) + (x >= thr ? (x == B ? ((y >> 16) & 0xffu) : 1u) : 0u);
+            if (x == B)
+                lone = int(y & 0xffffu);
         }
         return info;
     }
