@@ -1214,7 +1214,10 @@ struct St {
                         }
                     }
                     // @region gi_folds
-                    B = fmax(B, block_max_d(lb));
+                    int lone = 0;
+                    const u32 info = near_best(lb, eps2, q1, h1, q2, h2, ovf, B, lone);
+                    if (info == 1u && q_lo == 0 && q_hi == m)
+                        return lone;  // a lone near-best candidate is the pick: no fold, no argmax
                     const double thr = __dsub_rn(B, eps2);
                     if (ovf) {  // more than two near-ties in one thread: rescan
                         const double2 r = gi_rescan(ks, c, m, q_lo, q_hi, c0, T, alpha, beta, topmin, thr, best_s,
@@ -1569,27 +1572,7 @@ struct St {
         }
     }
 
-    __device__ __forceinline__ double block_max_d(double v) {
-        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 16));
-        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 8));
-        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 4));
-        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 2));
-        v = fmax(v, __shfl_xor_sync(FULLMASK, v, 1));
-        if (NW == 1)
-            return v;
-        rsel ^= 1;
-        double* r = sp<double>(lay.reds) + rsel * NW;
-        if (lane == 0)
-            r[tid >> 5] = v;
-        __syncthreads();
-        double b = r[0];
-#pragma unroll
-        for (int w = 1; w < NW; ++w)
-            b = fmax(b, r[w]);
-        return b;
-    }
-
-    // Dense gi pruning in one barrier: B = max(B, block max of lb) and the
+    // gi pruning (dense and walk) in one barrier: B = max(B, block max of lb) and the
     // near-best count (ovf flags << 16 | candidates >= B - eps2).  Each warp
     // publishes its max, its count relative to its own max and the index of
     // its max; a warp whose max is B counts exactly, another warp within the
