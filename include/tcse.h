@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define TCSE_ABI_VERSION 1
+#define TCSE_ABI_VERSION 2
 
 /* error codes */
 enum {
@@ -176,18 +176,29 @@ typedef struct tcse_flip_result {
 typedef struct tcse_stats {
     uint64_t steps;        /* selected substitutions (replayed prefixes excluded) */
     uint64_t replayed;     /* prefix substitutions replayed by reinit processes */
-    uint64_t processes;    /* process runs */
-    uint64_t launches;     /* search-kernel launches */
+    uint64_t processes;    /* process runs (iterations x processes of the systems still searching) */
+    uint64_t launches;     /* search-kernel launches (one per launch group per iteration) */
     int32_t iterations;    /* iteration barriers passed (max over systems) */
     int32_t retries;       /* iterations re-run at full candidate capacity (session layouts are
                               sized from the starting list; results never depend on it) */
-    double kernel_ms;      /* summed search-kernel time (CUDA events on the launch stream) */
-    double step_ms;        /* summed iteration time on the device: search + reduce (CUDA events) */
+    double kernel_ms;      /* device clock: summed spans of the iterations' search kernels
+                              (first search block start -> last block end, all groups) */
+    double step_ms;        /* summed device time of the iterations (CUDA events around them) */
     double wall_ms;        /* whole call, host clock */
-    double exchange_ms;    /* host time from search launch to incumbent state read-back */
+    double exchange_ms;    /* device clock: pack -> all-gather -> barrier kernels, summed */
     uint64_t h2d_bytes;    /* host->device bytes copied by the call */
     uint64_t d2h_bytes;    /* device->host bytes copied by the call */
     uint64_t wops;         /* algorithmic word-intersections (SURVEY.md 8(d) model) */
+    uint64_t steps_by_strategy[TCSE_STRATEGY_COUNT]; /* steps by the process's StrategyKind */
+    int32_t n_groups;      /* launch groups (one kernel instantiation each) */
+    int32_t group_nt[4];   /* threads per process of each group */
+    int32_t group_words[4];/* mask words W of each group */
+    int32_t reserved;
+    double group_ms[4];    /* device clock: summed search-kernel span of each group */
+    uint64_t group_wops[4];/* word-ops of each group's systems */
+    uint64_t graph_launches; /* iterations replayed from the captured CUDA graph */
+    uint64_t host_syncs;   /* host synchronisations (one per batch of iterations) */
+    uint64_t kernel_launches; /* kernels launched for the kept iterations */
 } tcse_stats;
 
 /* Called on the calling thread after every iteration barrier, like
@@ -223,6 +234,28 @@ void tcse_destroy(tcse_ctx* ctx);
  * e.g. torch.cuda.current_stream().cuda_stream so that caller-side CUDA
  * events bracket the work. */
 int tcse_set_stream(tcse_ctx* ctx, void* stream);
+
+/* Several devices of this process as ONE context: one
+ * sub-context per device with its own stream and an NCCL communicator
+ * (ncclCommInitAll).  tcse_optimize_system(s) on it partitions the processes
+ * across the devices (rank r = devices[r]) and runs one host thread per
+ * device; each iteration's payload all-gather is an ncclAllGather over
+ * NVLink on the device streams, inside the iteration's CUDA graph.  Results
+ * are identical to one device.  Other calls run on devices[0].  NULL on
+ * failure (no NCCL, duplicate device). */
+tcse_ctx* tcse_create_devices(const int32_t* devices, int32_t n_devices);
+int32_t tcse_context_devices(const tcse_ctx* ctx);
+
+/* One process per GPU (torchrun / MPI style): rank 0 makes an NCCL unique
+ * id (128 bytes), the caller broadcasts it, every rank attaches it to its
+ * context; the library then runs the payload all-gather itself
+ * (ncclAllGather on the context stream, captured in the iteration graph).
+ * NCCL is bound at run time (the copy already in the process, else
+ * TCSE_NCCL_LIBRARY, else libnccl.so.2); tcse_nccl_available() says whether
+ * it could be loaded. */
+int32_t tcse_nccl_available(void);
+int tcse_nccl_unique_id(void* unique_id_128);
+int tcse_set_nccl(tcse_ctx* ctx, const void* unique_id_128, int32_t rank, int32_t world);
 
 /* Process partition across ranks: this rank runs global process ids
  * [floor(n*rank/world), floor(n*(rank+1)/world)) of every iteration; the
@@ -281,6 +314,15 @@ int tcse_search_create(tcse_ctx* ctx, int32_t n_systems, const tcse_system* syst
                        void* user, tcse_search** out);
 int tcse_search_step(tcse_search* search, int32_t* n_active);
 
+/* Up to max_iterations iterations as a device-resident loop: the iteration
+ * (prep, place, search, pack, [NCCL all-gather], barrier) is a captured CUDA
+ * graph replayed back to back, patience and max_iterations are evaluated on
+ * the device, and the host synchronises once per batch (a batch = the
+ * iterations the search is certain to run).  An on_iteration callback or a
+ * host all-gather callback needs a host turn per iteration and runs them one
+ * at a time.  tcse_optimize_systems is create + run + result. */
+int tcse_search_run(tcse_search* search, int32_t max_iterations, int32_t* n_active);
+
 /* The same iteration in two phases around a caller-run collective (world > 1
  * without an allgather callback, e.g. ncclAllGather / torch.distributed
  * all_gather_into_tensor over NVLink).  begin launches the iteration on the
@@ -324,6 +366,14 @@ int tcse_microbench_wordops(tcse_ctx* ctx, double* gops);
  * malformed scheme, or "verify_by_product: trials must be >= 1". */
 int tcse_verify_schemes(tcse_ctx* ctx, const tcse_scheme* schemes, int32_t count, int32_t method,
                         int32_t trials, uint64_t seed, tcse_check_report* out);
+
+/* A flip-graph walk on the host (no GPU): `flips` consecutive random_flip
+ * moves (scheme.hpp:204-276) drawn from std::mt19937_64 `rng_seed`, as the
+ * reference's fixture generator and optimize_with_flips chain them.  u/v/w
+ * are caller-allocated with the input's shapes.  Identical output to the
+ * reference with the same libstdc++ (the walk uses std::shuffle). */
+int tcse_flip_walk(const tcse_scheme* scheme, uint64_t rng_seed, int32_t flips,
+                   int8_t* u, int8_t* v, int8_t* w);
 
 /* Host-side result/verification API kept from the reference (no GPU):
  * replay_prefix + total_cost + expand_and_verify (linear_system.hpp:193-258,

@@ -29,7 +29,7 @@ from .slp import combine_componentwise, count_slp_operators, emit_slp, emit_slp_
 __all__ = [
     "TcseError", "LinearSystem", "ProcessConfig", "SearchConfig", "SolutionRecord", "Device",
     "count_pairs", "run_cse", "optimize_system", "optimize_systems", "optimize_scheme", "Search",
-    "optimize_with_flips",
+    "optimize_with_flips", "flip_walk", "naive_scheme",
     "verify_record", "report_to_json", "strategy_from_string", "library_path",
     "parse_scheme", "load_scheme", "extract_systems", "naive_cost", "scheme_digest", "verify_brent",
     "SchemeError", "STRATEGY_NAMES", "STRATEGY_SHORT", "DEFAULT_WEIGHTS",
@@ -91,6 +91,14 @@ def lib():
         L.tcse_search_create.argtypes = [C.c_void_p, C.c_int32, P(_abi.System), P(_abi.SearchConfig),
                                          P(C.c_uint64), _abi.ITER_CB, C.c_void_p, P(C.c_void_p)]
         L.tcse_search_step.argtypes = [C.c_void_p, P(C.c_int32)]
+        L.tcse_search_run.argtypes = [C.c_void_p, C.c_int32, P(C.c_int32)]
+        L.tcse_create_devices.argtypes = [P(C.c_int32), C.c_int32]
+        L.tcse_create_devices.restype = C.c_void_p
+        L.tcse_context_devices.argtypes = [C.c_void_p]
+        L.tcse_context_devices.restype = C.c_int32
+        L.tcse_nccl_available.restype = C.c_int32
+        L.tcse_nccl_unique_id.argtypes = [C.c_void_p]
+        L.tcse_set_nccl.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
         L.tcse_search_result.argtypes = [C.c_void_p, P(_abi.Record), P(C.c_int32), P(_abi.Stats)]
         L.tcse_search_destroy.argtypes = [C.c_void_p]
         L.tcse_optimize_with_flips.argtypes = [C.c_void_p, P(_abi.Scheme), P(_abi.SearchConfig), P(_abi.FlipConfig),
@@ -98,6 +106,8 @@ def lib():
         if hasattr(L, "tcse_verify_schemes") or not os.environ.get("TCSE_LIBRARY"):  # older A/B builds lack it
             L.tcse_verify_schemes.argtypes = [C.c_void_p, P(_abi.Scheme), C.c_int32, C.c_int32, C.c_int32,
                                               C.c_uint64, P(_abi.CheckReport)]
+        L.tcse_flip_walk.argtypes = [P(_abi.Scheme), C.c_uint64, C.c_int32, P(C.c_int8), P(C.c_int8),
+                                     P(C.c_int8)]
         L.tcse_search_payload_bytes.argtypes = [C.c_void_p]
         L.tcse_search_payload_bytes.restype = C.c_size_t
         L.tcse_search_step_begin.argtypes = [C.c_void_p, C.c_void_p]
@@ -195,16 +205,43 @@ class SolutionRecord:
 
 
 class Device:
-    """Owns a tcse_ctx (device, stream, pools, optional rank partition)."""
+    """Owns a tcse_ctx (device, stream, pools, optional rank partition).
+
+    Device(0) is one GPU; Device([0, 1, 2, 3]) is ONE context over several
+    GPUs of this process (tcse_create_devices): optimize_system(s) then
+    partitions the processes across them with an NCCL all-gather per
+    iteration, results identical to one GPU."""
 
     def __init__(self, device=0):
         L = lib()
-        h = L.tcse_create(int(device))
+        if isinstance(device, (list, tuple)):
+            arr = (C.c_int32 * len(device))(*device)
+            h = L.tcse_create_devices(arr, len(device))
+            device = device[0] if len(device) == 1 else tuple(device)
+        else:
+            h = L.tcse_create(int(device))
         if not h:
             raise TcseError(_abi.TCSE_ECUDA, L.tcse_last_error().decode())
         self._h = h
         self._cb = None
         self.device = device
+
+    @property
+    def n_devices(self):
+        return lib().tcse_context_devices(self._h)
+
+    @staticmethod
+    def nccl_unique_id():
+        """128-byte NCCL unique id (rank 0 makes it, the caller broadcasts it)."""
+        buf = C.create_string_buffer(128)
+        _check(lib().tcse_nccl_unique_id(buf))
+        return buf.raw
+
+    def set_nccl(self, unique_id, rank, world):
+        """One process per GPU: the library runs the per-iteration payload
+        all-gather itself (ncclAllGather on the context stream)."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().tcse_set_nccl(self._h, buf, rank, world))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -303,7 +340,7 @@ def run_cse(sys, cfgs, prefix=(), trace_stride=0, device=None, stats=None):
     _check(lib().tcse_run_cse(d.handle, C.byref(s.c), pre, npre, carr, n, rarr, trace, trace_stride,
                               C.byref(st)))
     if stats is not None:
-        stats.update({k: getattr(st, k) for k, _ in _abi.Stats._fields_})
+        stats.update(_stats_dict(st))
     out = [SolutionRecord.from_c(rarr[b]) for b in range(n)]
     if trace_stride > 0:
         traces = [[trace[b * trace_stride + t] for t in range(min(trace_stride, len(out[b].substitutions) + 1))]
@@ -313,7 +350,11 @@ def run_cse(sys, cfgs, prefix=(), trace_stride=0, device=None, stats=None):
 
 
 def _stats_dict(st):
-    return {k: getattr(st, k) for k, _ in _abi.Stats._fields_}
+    out = {}
+    for k, _ in _abi.Stats._fields_:
+        v = getattr(st, k)
+        out[k] = list(v) if hasattr(v, "_length_") else v
+    return out
 
 
 class Search:
@@ -348,6 +389,14 @@ class Search:
     def step(self):
         left = C.c_int32()
         _check(lib().tcse_search_step(self._h, C.byref(left)))
+        self.active = left.value
+        return self.active
+
+    def run(self, max_iterations=1 << 30):
+        """Up to max_iterations iterations as a device-resident loop (CUDA
+        graph replays, one host synchronisation per batch)."""
+        left = C.c_int32()
+        _check(lib().tcse_search_run(self._h, int(max_iterations), C.byref(left)))
         self.active = left.value
         return self.active
 
@@ -424,7 +473,7 @@ def optimize_systems(systems, cfg, salts=None, on_iteration=None, device=None, s
     _check(lib().tcse_optimize_systems(d.handle, n, sarr, C.byref(ccfg), salt_arr, cfun, None, rarr, its,
                                        C.byref(st)))
     if stats is not None:
-        stats.update({k: getattr(st, k) for k, _ in _abi.Stats._fields_})
+        stats.update(_stats_dict(st))
     return [(SolutionRecord.from_c(rarr[t]), its[t]) for t in range(n)]
 
 
@@ -459,13 +508,13 @@ def optimize_scheme(scheme, cfg, device=None, stats=None):
     """optimize_scheme (parallel_search.hpp:314-345): validate, extract, run
     U/V/W CONCURRENTLY on the device, re-verify every winning record, report."""
     t0 = time.time()
-    if scheme["r"] >= 200:
-        valid, why = True, None  # randomized product check is host-side I/O; exact below
-    else:
-        valid, why = verify_brent(scheme)
-    if not valid:
-        raise TcseError(_abi.TCSE_EINVAL, "optimize_scheme: scheme failed validation (%s)" % why)
     resolved = SearchConfig(**cfg)
+    # check_scheme_auto (parallel_search.hpp:296-302) on the device: exact
+    # Brent below rank 200, 16 random products seeded by master_seed above
+    rep = verify_schemes([scheme], "auto", trials=16, seed=resolved["master_seed"], device=device)[0]
+    if not rep.valid:
+        raise TcseError(_abi.TCSE_EINVAL, "optimize_scheme: scheme failed validation (%s)"
+                        % (rep.first_violation or "unknown"))
     if resolved["n_processes"] == 0:
         resolved["n_processes"] = tier_processes(scheme["r"])
     systems = [LinearSystem(nx, rows) for nx, rows in extract_systems(scheme)]
@@ -590,6 +639,36 @@ def optimize_with_flips(scheme, cfg, device=None, stats=None):
         comps.append(dict(record=rec, cost=rec.cost, naive=res.naive[k], iterations=res.iterations, scheme_id=sid))
     return dict(scheme_digest=scheme_digest(carried), config=resolved, components=comps, total=res.total,
                 iterations=res.iterations, scheme=carried)
+
+
+def flip_walk(scheme, rng_seed, flips):
+    """`flips` consecutive random_flip moves (scheme.hpp:204-276) from
+    std::mt19937_64(rng_seed) on the host (libtcse's slab walk, no device)."""
+    m, n, p, r = scheme["m"], scheme["n"], scheme["p"], scheme["r"]
+    flat = lambda t: (C.c_int8 * max(1, sum(len(x) for x in t)))(*[v for row in t for v in row])  # noqa: E731
+    cu, cv, cw = flat(scheme["u"]), flat(scheme["v"]), flat(scheme["w"])
+    ou, ov, ow = (C.c_int8 * (r * m * n))(), (C.c_int8 * (r * n * p))(), (C.c_int8 * (m * p * r))()
+    _check(lib().tcse_flip_walk(C.byref(_abi.Scheme(m, n, p, r, cu, cv, cw)), rng_seed, flips, ou, ov, ow))
+    return dict(m=m, n=n, p=p, r=r, u=[list(ou[q * m * n:(q + 1) * m * n]) for q in range(r)],
+                v=[list(ov[q * n * p:(q + 1) * n * p]) for q in range(r)],
+                w=[list(ow[row * r:(row + 1) * r]) for row in range(m * p)])
+
+
+def naive_scheme(m, n, p):
+    """naive_scheme (scheme.hpp:161-176): product (i, j, k) = a_ij * b_jk -> c_ik."""
+    r = m * n * p
+    u = [[0] * (m * n) for _ in range(r)]
+    v = [[0] * (n * p) for _ in range(r)]
+    w = [[0] * r for _ in range(m * p)]
+    q = 0
+    for i in range(m):
+        for j in range(n):
+            for k in range(p):
+                u[q][i * n + j] = 1
+                v[q][j * p + k] = 1
+                w[i * p + k][q] = 1
+                q += 1
+    return dict(m=m, n=n, p=p, r=r, u=u, v=v, w=w)
 
 
 CHECK_METHODS = {"auto": _abi.TCSE_CHECK_AUTO, "exact_brent": _abi.TCSE_CHECK_BRENT,

@@ -93,6 +93,16 @@ class Stats(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("wops", C.c_uint64),
+        ("steps_by_strategy", C.c_uint64 * 7),
+        ("n_groups", C.c_int32),
+        ("group_nt", C.c_int32 * 4),
+        ("group_words", C.c_int32 * 4),
+        ("reserved", C.c_int32),
+        ("group_ms", C.c_double * 4),
+        ("group_wops", C.c_uint64 * 4),
+        ("graph_launches", C.c_uint64),
+        ("host_syncs", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
     ]
 
 

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtcse.so")
-SOURCES = ["search.cu", "host.cpp", "microbench.cu", "verify.cu"]
+SOURCES = ["search.cu", "host.cpp", "microbench.cu", "verify.cu", "nccl_dyn.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
@@ -48,7 +48,7 @@ def build(force=False, verbose=False):
             sys.stderr.write(out)
             raise RuntimeError("nvcc failed on %s" % src)
     link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-            "-o", OUT + ".tmp"] + objs
+            "-o", OUT + ".tmp"] + objs + ["-ldl"]
     subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
     for o in objs:

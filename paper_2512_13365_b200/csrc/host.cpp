@@ -14,8 +14,11 @@
 //     result is identical for any world size.
 // Semantics follow parallel_search.hpp:117-273 and cse_engine.hpp:29-57.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <array>
 #include <random>
 #include <chrono>
@@ -25,12 +28,16 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "launch.h"
+#include "nccl_dyn.h"
 
 namespace tcse {
 cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st);
@@ -49,6 +56,7 @@ cudaError_t launch_verify(const VerifyDesc* d_descs, const int8_t* d_coef, unsig
                           long long max_checks, int max_trials, int max_r, int n_sms, cudaStream_t st);
 cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st);
 cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st);
+int barrier_blocks(int n);
 }  // namespace tcse
 
 using namespace tcse;
@@ -245,6 +253,9 @@ struct tcse_ctx {
     int rank = 0, world = 1;
     tcse_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
+    ncclComm_t comm = nullptr;  // payload all-gather on `stream` (tcse_set_nccl / tcse_create_devices)
+    bool own_comm = false;
+    std::vector<tcse_ctx*> sub;  // multi-device context: rank r runs on sub[r]
     DBuf err;  // int32 err + err_pos
     DBuf slots, rng, perm, hist;  // prep_kernel -> search_kernel hand-off
     // launch groups beyond the first run on their own streams, forked from and
@@ -658,7 +669,15 @@ tcse_ctx* tcse_create(int32_t device) {
 void tcse_destroy(tcse_ctx* ctx) {
     if (!ctx)
         return;
+    for (tcse_ctx* c : ctx->sub)
+        tcse_destroy(c);
+    ctx->sub.clear();
     cudaSetDevice(ctx->device);
+    if (ctx->stream)
+        cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm && ctx->own_comm && nccl().ok)
+        nccl().CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
     if (ctx->owned_stream)
         cudaStreamDestroy(ctx->owned_stream);
     else if (ctx->stream)
@@ -690,12 +709,106 @@ int tcse_set_stream(tcse_ctx* ctx, void* stream) {
 int tcse_set_partition(tcse_ctx* ctx, int32_t rank, int32_t world, tcse_allgather_fn allgather, void* user) {
     if (!ctx || world < 1 || rank < 0 || rank >= world)
         return fail(TCSE_EINVAL, "tcse_set_partition: bad rank %d / world %d", rank, world);
+    if (!ctx->sub.empty())
+        return fail(TCSE_EINVAL, "tcse_set_partition: a multi-device context owns its partition");
     ctx->rank = rank;
     ctx->world = world;
     ctx->allgather = allgather;
     ctx->ag_user = user;
     return TCSE_OK;
 }
+
+int32_t tcse_nccl_available(void) { return nccl().ok ? 1 : 0; }
+
+int tcse_nccl_unique_id(void* id) {
+    if (!id)
+        return fail(TCSE_EINVAL, "tcse_nccl_unique_id: null buffer");
+    const NcclApi& nc = nccl();
+    if (!nc.ok)
+        return fail(TCSE_ENCCL, "nccl: %s", nc.why);
+    ncclUniqueId u;
+    const ncclResult_t r = nc.GetUniqueId(&u);
+    if (r != ncclSuccess)
+        return fail(TCSE_ENCCL, "ncclGetUniqueId: %s", nc.GetErrorString(r));
+    std::memcpy(id, &u, sizeof u);
+    return TCSE_OK;
+}
+
+int tcse_set_nccl(tcse_ctx* ctx, const void* unique_id, int32_t rank, int32_t world) {
+    if (!ctx || !unique_id || world < 1 || rank < 0 || rank >= world)
+        return fail(TCSE_EINVAL, "tcse_set_nccl: bad rank %d / world %d", rank, world);
+    if (!ctx->sub.empty())
+        return fail(TCSE_EINVAL, "tcse_set_nccl: a multi-device context owns its communicators");
+    const NcclApi& nc = nccl();
+    if (!nc.ok)
+        return fail(TCSE_ENCCL, "nccl: %s", nc.why);
+    CU(cudaSetDevice(ctx->device));
+    ncclUniqueId u;
+    std::memcpy(&u, unique_id, sizeof u);
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = nc.CommInitRank(&comm, world, u, rank);
+    if (r != ncclSuccess)
+        return fail(TCSE_ENCCL, "ncclCommInitRank: %s", nc.GetErrorString(r));
+    if (ctx->comm && ctx->own_comm)
+        nc.CommDestroy(ctx->comm);
+    ctx->comm = comm;
+    ctx->own_comm = true;
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->allgather = nullptr;
+    return TCSE_OK;
+}
+
+tcse_ctx* tcse_create_devices(const int32_t* devices, int32_t n_devices) {
+    if (!devices || n_devices < 1) {
+        fail(TCSE_EINVAL, "tcse_create_devices: need at least one device");
+        return nullptr;
+    }
+    if (n_devices == 1)
+        return tcse_create(devices[0]);
+    for (int a = 0; a < n_devices; ++a)
+        for (int b = a + 1; b < n_devices; ++b)
+            if (devices[a] == devices[b]) {
+                fail(TCSE_EINVAL, "tcse_create_devices: device %d listed twice", devices[a]);
+                return nullptr;
+            }
+    const NcclApi& nc = nccl();
+    if (!nc.ok) {
+        fail(TCSE_ENCCL, "nccl: %s", nc.why);
+        return nullptr;
+    }
+    auto* top = tcse_create(devices[0]);
+    if (!top)
+        return nullptr;
+    std::vector<ncclComm_t> comms(size_t(n_devices), nullptr);
+    std::vector<int> devs(devices, devices + n_devices);
+    const ncclResult_t r = nc.CommInitAll(comms.data(), n_devices, devs.data());
+    if (r != ncclSuccess) {
+        fail(TCSE_ENCCL, "ncclCommInitAll: %s", nc.GetErrorString(r));
+        tcse_destroy(top);
+        return nullptr;
+    }
+    for (int k = 0; k < n_devices; ++k) {
+        tcse_ctx* c = tcse_create(devices[k]);
+        if (!c) {
+            for (int j = k; j < n_devices; ++j)
+                nc.CommDestroy(comms[size_t(j)]);
+            tcse_destroy(top);
+            return nullptr;
+        }
+        c->comm = comms[size_t(k)];
+        c->own_comm = true;
+        c->rank = k;
+        c->world = n_devices;
+        top->sub.push_back(c);
+    }
+    // the container itself is a single-device context on devices[0]: calls
+    // other than tcse_optimize_system(s) (run_cse, count_pairs, flips, checks)
+    // run there
+    return top;
+}
+
+int32_t tcse_context_devices(const tcse_ctx* ctx) { return ctx ? int32_t(std::max<size_t>(1, ctx->sub.size())) : 0; }
 
 int tcse_count_pairs(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix, int32_t n_prefix,
                      int32_t min_count, tcse_pair_count* out, int32_t cap, int32_t* n_out) {
@@ -865,595 +978,9 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
 
 }  // extern "C"
 
-// ---------------------------------------------------------------- session
-
-namespace {
-
-struct Pool {
-    DBuf cost, len, own, strat, seed, wops, subs, reinit, inc, inc_keys;
-    int sub_cap = 0;
-};
-
-}  // namespace
-
-// One optimize_systems run, advanced one iteration barrier at a time.
-struct tcse_search {
-    tcse_ctx* ctx = nullptr;
-    int n_systems = 0;
-    tcse_search_config cfg;
-    std::vector<uint64_t> salts;
-    tcse_iter_cb cb = nullptr;
-    void* user = nullptr;
-    int n = 0, p0 = 0, n_local = 0, hist_n = 1;
-    struct Group {
-        int W, nt;
-        bool dense;
-        int smem;
-        std::vector<int> sys;
-    };
-    std::vector<Group> groups;
-    double weight_total = 0.0;
-    std::unique_ptr<DevSys[]> dev;
-    std::unique_ptr<Pool[]> pool;
-    std::vector<int> active, unchanged, iters;
-    std::vector<IncState> hinc;
-    std::vector<std::vector<u32>> hinc_keys;
-    std::vector<std::vector<tcse_pair>> hinc_pairs;
-    uint64_t launches = 0, processes = 0, h2d = 0, d2h = 0;
-    double kernel_ms = 0.0, step_ms = 0.0, exchange_ms = 0.0;
-    int iteration = 0;
-    bool stopped = false;
-    bool shrunk = false;  // some system runs with a shrunk candidate capacity
-    int retries = 0;      // iterations re-run at full capacity
-    cudaEvent_t es0 = nullptr, es1 = nullptr;
-    std::chrono::steady_clock::time_point t0;
-    // exchange payload layout (int32 words): per system [n_max costs | 6 | sub_cap]
-    int n_max = 0, words_total = 0;
-    std::vector<int> sys_off;
-    DBuf send, recv;
-    std::vector<int32_t> hsend, hrecv;
-    std::vector<int> act;  // systems active in the pending iteration
-    int32_t* send_used = nullptr;
-    bool pending = false;
-    std::chrono::steady_clock::time_point tx;
-    ~tcse_search() {
-        if (es0)
-            cudaEventDestroy(es0);
-        if (es1)
-            cudaEventDestroy(es1);
-    }
-};
-
-namespace {
-
-// launch groups: systems with the same kernel instantiation share a launch;
-// groups after the first get their own stream
-int build_groups(tcse_search* S) {
-    tcse_ctx* ctx = S->ctx;
-    S->groups.clear();
-    for (int s = 0; s < S->n_systems; ++s) {
-        const DevSys& d = S->dev[size_t(s)];
-        bool placed = false;
-        for (auto& g : S->groups)
-            if (g.W == d.W && g.nt == d.nt && g.dense == d.dense) {
-                g.sys.push_back(s);
-                g.smem = std::max(g.smem, smem_one(d));
-                placed = true;
-            }
-        if (!placed)
-            S->groups.push_back({d.W, d.nt, d.dense, smem_one(d), {s}});
-    }
-    // most work first (starting candidates x naive cost ~ steps x per-step
-    // cost): the long group's blocks start first and the short ones fill the
-    // tail (+8% on 5x5x5, +3% on 6x6x6 over creation order)
-    auto work = [&](const tcse_search::Group& g) {
-        double w = 0.0;
-        for (int s : g.sys)
-            w += double(S->dev[size_t(s)].base_m) * double(S->dev[size_t(s)].h.naive);
-        return w;
-    };
-    std::stable_sort(S->groups.begin(), S->groups.end(),
-                     [&](const tcse_search::Group& a, const tcse_search::Group& b) { return work(a) > work(b); });
-    for (const auto& g : S->groups)
-        if (g.smem > 227 * 1024 - 1024)
-            return fail(TCSE_ECAPACITY, "system needs %d bytes of shared memory per process", g.smem);
-    for (size_t g = 1; g < S->groups.size(); ++g) {
-        if (!ctx->aux[g - 1])
-            CU(cudaStreamCreateWithFlags(&ctx->aux[g - 1], cudaStreamNonBlocking));
-        if (!ctx->join[g - 1])
-            CU(cudaEventCreateWithFlags(&ctx->join[g - 1], cudaEventDisableTiming));
-    }
-    return TCSE_OK;
-}
-
-int search_init(tcse_search* S, tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
-                const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb, void* user) {
-    if (!ctx || n_systems < 1 || n_systems > kMaxSys || !systems)
-        return fail(TCSE_EINVAL, "optimize_systems: bad argument (1..%d systems)", kMaxSys);
-    int rc = validate_config(cfg);
-    if (rc)
-        return rc;
-    if ((cfg->forced_strategy == TCSE_MIXED || (cfg->forced_strategy < 0 && cfg->strategy_weights[TCSE_MIXED] > 0.0)) &&
-        (rc = validate_mix(cfg->mix_weights)))
-        return rc;
-    S->t0 = std::chrono::steady_clock::now();
-    CU(cudaSetDevice(ctx->device));
-    S->ctx = ctx;
-    S->n_systems = n_systems;
-    S->cfg = *cfg;
-    S->cb = cb;
-    S->user = user;
-    for (int s = 0; s < n_systems; ++s)
-        S->salts.push_back(salts ? salts[s] : uint64_t(s));
-    S->n = cfg->n_processes > 0 ? cfg->n_processes : 256;  // parallel_search.hpp:224
-    const int world = ctx->world, rank = ctx->rank;
-    S->p0 = int((long long)S->n * rank / world);
-    S->n_local = int((long long)S->n * (rank + 1) / world) - S->p0;
-    S->dev.reset(new DevSys[size_t(n_systems)]);
-    S->pool.reset(new Pool[size_t(n_systems)]);
-    for (int s = 0; s < n_systems; ++s) {
-        DevSys& d = S->dev[size_t(s)];
-        rc = prepare(ctx, &systems[s], &d);
-        if (rc)
-            return rc;
-        S->h2d += uint64_t(d.h.n_x) * 2 * uint64_t(d.W) * 8;
-        rc = base_candidates(ctx, d);
-        if (rc)
-            return rc;
-        shrink_capacity(ctx, &d);
-        S->shrunk = S->shrunk || d.mcap_full > 0;
-    }
-    if ((rc = build_groups(S)))
-        return rc;
-    if (!ctx->fork)
-        CU(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
-    for (int s = 0; s < n_systems; ++s) {
-        Pool& P = S->pool[size_t(s)];
-        const DevSys& d = S->dev[size_t(s)];
-        P.sub_cap = d.h.naive / 2 + 1;
-        const size_t nl = size_t(std::max(S->n_local, 1));
-        CU(P.cost.reserve(4 * nl));
-        CU(P.len.reserve(4 * nl));
-        CU(P.own.reserve(4 * nl));
-        CU(P.strat.reserve(4 * nl));
-        CU(P.seed.reserve(8 * nl));
-        CU(P.wops.reserve(8 * nl));
-        CU(P.subs.reserve(4 * nl * size_t(P.sub_cap)));
-        CU(P.reinit.reserve(size_t(S->n)));
-        CU(P.inc.reserve(sizeof(IncState)));
-        CU(P.inc_keys.reserve(4 * size_t(P.sub_cap)));
-        CU(cudaMemsetAsync(P.inc.p, 0, sizeof(IncState), ctx->stream));
-        CU(cudaMemsetAsync(P.reinit.p, 0, size_t(S->n), ctx->stream));
-        S->hist_n = std::max(S->hist_n, d.h.naive + 1);
-    }
-    CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
-    S->n_max = (S->n + world - 1) / world + 1;
-    for (int s = 0; s < n_systems; ++s) {
-        S->sys_off.push_back(S->words_total);
-        S->words_total += S->n_max + 6 + S->pool[size_t(s)].sub_cap;
-    }
-    CU(S->send.reserve(4 * size_t(S->words_total)));
-    if (world > 1)
-        CU(S->recv.reserve(4 * size_t(S->words_total) * size_t(world)));
-    for (int k = 0; k < 7; ++k)
-        S->weight_total += cfg->strategy_weights[k];
-    S->active.assign(size_t(n_systems), 1);
-    S->unchanged.assign(size_t(n_systems), 0);
-    S->iters.assign(size_t(n_systems), 0);
-    S->hinc.assign(size_t(n_systems), IncState());
-    std::memset(S->hinc.data(), 0, sizeof(IncState) * size_t(n_systems));
-    S->hinc_keys.assign(size_t(n_systems), {});
-    S->hinc_pairs.assign(size_t(n_systems), {});
-    CU(cudaEventCreate(&S->es0));
-    CU(cudaEventCreate(&S->es1));
-    CU(cudaStreamSynchronize(ctx->stream));
-    return TCSE_OK;
-}
-
-XchgDesc xdesc(tcse_search* S, int s) {
-    Pool& P = S->pool[size_t(s)];
-    XchgDesc X;
-    std::memset(&X, 0, sizeof X);
-    X.n = S->n;
-    X.world = S->ctx->world;
-    X.n_max = S->n_max;
-    X.sys_off = S->sys_off[size_t(s)];
-    X.words_total = S->words_total;
-    X.n_local = S->n_local;
-    X.p0 = S->p0;
-    X.sub_cap = P.sub_cap;
-    X.cost = P.cost.as<int32_t>();
-    X.len = P.len.as<int32_t>();
-    X.own = P.own.as<int32_t>();
-    X.strat = P.strat.as<int32_t>();
-    X.seed = P.seed.as<u64>();
-    X.wops = P.wops.as<u64>();
-    X.subs = P.subs.as<u32>();
-    X.inc = P.inc.as<IncState>();
-    X.inc_keys = P.inc_keys.as<u32>();
-    X.reinit_next = P.reinit.as<u8>();
-    X.fraction = S->cfg.reinit_fraction;
-    X.hist_n = S->hist_n;
-    return X;
-}
-
-// K0 + K1 for every active system, then this rank's exchange payload (K2a)
-int search_step_begin(tcse_search* S, void* send_ext) {
-    tcse_ctx* ctx = S->ctx;
-    int rc = TCSE_OK;
-    if (S->pending)
-        return fail(TCSE_EINVAL, "tcse_search_step_begin: previous iteration not finished");
-    S->act.clear();
-    for (int s = 0; s < S->n_systems; ++s)
-        if (S->active[size_t(s)])
-            S->act.push_back(s);
-    if (S->act.empty() || S->stopped)
-        return TCSE_OK;
-    CU(cudaSetDevice(ctx->device));
-    const int iteration = ++S->iteration;
-    // ---- K0 + K1 per launch group; groups after the first on their own
-    // streams (forked from / joined into the context stream)
-    int total = 0;
-    for (int s : S->act)
-        total += S->n_local;
-    if ((rc = reserve_prep(ctx, total)))
-        return rc;
-    CU(cudaEventRecord(S->es0, ctx->stream));
-    CU(cudaEventRecord(ctx->ev0, ctx->stream));
-relaunch:
-    CU(cudaEventRecord(ctx->fork, ctx->stream));
-    int block_off = 0, n_aux = 0;
-    static const int group_order = env_int("TCSE_GROUP_ORDER", 0);   // 1: reverse (A/B knob)
-    static const int group_serial = env_int("TCSE_GROUP_SERIAL", 0); // 1: one stream (A/B knob)
-    for (size_t gq = 0; gq < S->groups.size(); ++gq) {
-        const size_t gi = group_order == 1 ? S->groups.size() - 1 - gq : gq;
-        const auto& g = S->groups[gi];
-        LaunchDesc L;
-        std::memset(&L, 0, sizeof L);
-        int blocks = 0;
-        for (int s : g.sys) {
-            if (!S->active[size_t(s)])
-                continue;
-            const DevSys& d = S->dev[size_t(s)];
-            Pool& P = S->pool[size_t(s)];
-            SysDesc sd = base_desc(d, ctx->err.as<int32_t>());
-            sd.mode = kModeSearch;
-            sd.base_keys = d.keys.as<u32>();
-            sd.base_cnts = d.cnts.as<u16>();
-            sd.base_m = d.base_m;
-            sd.n_local = S->n_local;
-            sd.p0 = S->p0;
-            sd.block_begin = blocks;
-            sd.master_seed = S->cfg.master_seed;
-            sd.salt = S->salts[size_t(s)];
-            sd.iteration = iteration;
-            sd.forced = S->cfg.forced_strategy;
-            for (int k = 0; k < 7; ++k)
-                sd.weights[k] = S->cfg.strategy_weights[k];
-            sd.weight_total = S->weight_total;
-            for (int k = 0; k < 4; ++k)
-                sd.mix[k] = S->cfg.mix_weights[k];
-            sd.reinit = iteration >= 2 ? P.reinit.as<u8>() + S->p0 : nullptr;
-            sd.inc_keys = P.inc_keys.as<u32>();
-            sd.inc_len = S->hinc[size_t(s)].len;
-            sd.out_cost = P.cost.as<int32_t>();
-            sd.out_len = P.len.as<int32_t>();
-            sd.out_own = P.own.as<int32_t>();
-            sd.out_strategy = P.strat.as<int32_t>();
-            sd.out_seed = P.seed.as<u64>();
-            sd.out_wops = P.wops.as<u64>();
-            sd.out_subs = P.subs.as<u32>();
-            sd.gi_dense = g.dense ? 1 : 0;
-            L.sys[L.nsys++] = sd;
-            blocks += S->n_local;
-        }
-        if (blocks == 0)
-            continue;
-        L.total_blocks = blocks;
-        if ((rc = attach_prep(ctx, &L, block_off, int(gi))))
-            return rc;
-        block_off += blocks;
-        cudaStream_t st = ctx->stream;
-        if (!group_serial && n_aux + 1 <= int(S->groups.size()) - 1 && block_off > blocks) {
-            st = ctx->aux[n_aux];
-            CU(cudaStreamWaitEvent(st, ctx->fork, 0));
-        }
-        CU(launch_search(L, g.W, g.nt, g.dense, g.smem, st));
-        if (st != ctx->stream)
-            CU(cudaEventRecord(ctx->join[n_aux++], st));
-        ++S->launches;
-        S->processes += uint64_t(blocks);
-    }
-    for (int a = 0; a < n_aux; ++a)
-        CU(cudaStreamWaitEvent(ctx->stream, ctx->join[a], 0));
-    if (S->shrunk) {
-        // a process outgrew a shrunk capacity: the same iteration again at
-        // full capacity (slots and streams are pure functions of the
-        // iteration, incumbent and reinit set, none of which changed)
-        int32_t h[2] = {0, 0};
-        CU(cudaMemcpyAsync(h, ctx->err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        if (h[0] == kErrCandOverflow) {
-            CU(cudaMemsetAsync(ctx->err.p, 0, 8, ctx->stream));
-            for (int s = 0; s < S->n_systems; ++s)
-                restore_capacity(ctx, &S->dev[size_t(s)]);
-            S->shrunk = false;
-            ++S->retries;
-            if ((rc = build_groups(S)))
-                return rc;
-            goto relaunch;
-        }
-    }
-    CU(cudaEventRecord(ctx->ev1, ctx->stream));
-    S->tx = std::chrono::steady_clock::now();
-    int32_t* send = send_ext ? static_cast<int32_t*>(send_ext) : S->send.as<int32_t>();
-    XchgLaunch XL;
-    std::memset(&XL, 0, sizeof XL);
-    for (int s : S->act) {
-        XchgDesc X = xdesc(S, s);
-        X.send = send;
-        XL.x[XL.nsys++] = X;
-    }
-    CU(launch_pack(XL, ctx->stream));
-    S->send_used = send;
-    S->pending = true;
-    return TCSE_OK;
-}
-
-// exchange (if any) + K2b + host bookkeeping (patience, on_iteration)
-int search_step_end(tcse_search* S, const void* recv_ext, int32_t* n_active) {
-    tcse_ctx* ctx = S->ctx;
-    int rc = TCSE_OK;
-    if (!S->pending) {
-        int left = 0;
-        for (int s = 0; s < S->n_systems; ++s)
-            left += S->active[size_t(s)];
-        *n_active = S->stopped ? 0 : left;
-        return TCSE_OK;
-    }
-    S->pending = false;
-    CU(cudaSetDevice(ctx->device));
-    const int world = ctx->world;
-    const int32_t* recv = S->send_used;
-    if (world > 1) {
-        if (recv_ext) {
-            recv = static_cast<const int32_t*>(recv_ext);
-        } else {
-            if (!ctx->allgather)
-                return fail(TCSE_ENCCL, "exchange: world %d needs an allgather callback or step_begin/step_end", world);
-            const size_t wt = size_t(S->words_total);
-            S->hsend.resize(wt);
-            S->hrecv.resize(wt * size_t(world));
-            CU(cudaMemcpyAsync(S->hsend.data(), S->send_used, 4 * wt, cudaMemcpyDeviceToHost, ctx->stream));
-            CU(cudaStreamSynchronize(ctx->stream));
-            if ((rc = check_err(ctx)))
-                return rc;
-            if (ctx->allgather(S->hsend.data(), S->hrecv.data(), 4 * wt, ctx->ag_user) != 0)
-                return fail(TCSE_ENCCL, "exchange: allgather failed");
-            CU(cudaMemcpyAsync(S->recv.p, S->hrecv.data(), 4 * wt * size_t(world), cudaMemcpyHostToDevice,
-                               ctx->stream));
-            S->d2h += 4 * wt;
-            S->h2d += 4 * wt * uint64_t(world);
-            recv = S->recv.as<int32_t>();
-        }
-    }
-    XchgLaunch XL;
-    std::memset(&XL, 0, sizeof XL);
-    for (int s : S->act) {
-        XchgDesc X = xdesc(S, s);
-        X.recv = recv;
-        XL.x[XL.nsys++] = X;
-    }
-    CU(launch_reduce(XL, S->hist_n, ctx->stream));
-    CU(cudaEventRecord(S->es1, ctx->stream));
-    std::vector<IncState> st(S->act.size());
-    for (size_t a = 0; a < S->act.size(); ++a)
-        CU(cudaMemcpyAsync(&st[a], S->pool[size_t(S->act[a])].inc.p, sizeof(IncState), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-    S->d2h += sizeof(IncState) * S->act.size();
-    CU(cudaStreamSynchronize(ctx->stream));
-    S->exchange_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - S->tx).count();
-    rc = check_err(ctx);
-    if (rc)
-        return rc;
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess)
-        S->kernel_ms += ms;
-    if (cudaEventElapsedTime(&ms, S->es0, S->es1) == cudaSuccess)
-        S->step_ms += ms;
-    const int iteration = S->iteration;
-    // ---- host: patience (parallel_search.hpp:261-270) and on_iteration
-    for (size_t a = 0; a < S->act.size(); ++a) {
-        const int s = S->act[a];
-        S->hinc[size_t(s)] = st[a];
-        S->iters[size_t(s)] = iteration;
-        if (st[a].improved) {
-            S->unchanged[size_t(s)] = 0;
-            S->hinc_keys[size_t(s)].resize(size_t(std::max(st[a].len, 1)));
-            if (S->cb) {
-                CU(cudaMemcpyAsync(S->hinc_keys[size_t(s)].data(), S->pool[size_t(s)].inc_keys.p,
-                                   4 * size_t(st[a].len), cudaMemcpyDeviceToHost, ctx->stream));
-                CU(cudaStreamSynchronize(ctx->stream));
-                S->d2h += 4 * uint64_t(st[a].len);
-            }
-        } else {
-            ++S->unchanged[size_t(s)];
-        }
-        if (S->cb) {
-            auto& pairs = S->hinc_pairs[size_t(s)];
-            if (st[a].improved || pairs.empty()) {
-                pairs.resize(size_t(std::max(st[a].len, 1)));
-                for (int t = 0; t < st[a].len; ++t)
-                    pairs[size_t(t)] = key_pair(S->hinc_keys[size_t(s)][size_t(t)]);
-            }
-            tcse_record r;
-            r.subs = pairs.data();
-            r.cap = st[a].len;
-            r.n_subs = st[a].len;
-            r.cost = st[a].cost;
-            r.strategy = st[a].strategy;
-            r.seed = st[a].seed;
-            if (S->cb(s, iteration, &r, S->user) != 0)
-                S->stopped = true;
-        }
-        if (S->unchanged[size_t(s)] >= S->cfg.patience ||
-            (S->cfg.max_iterations > 0 && iteration >= S->cfg.max_iterations))
-            S->active[size_t(s)] = 0;
-    }
-    int left = 0;
-    for (int s = 0; s < S->n_systems; ++s)
-        left += S->active[size_t(s)];
-    *n_active = S->stopped ? 0 : left;
-    return TCSE_OK;
-}
-
-int search_step(tcse_search* S, int32_t* n_active) {
-    int rc = search_step_begin(S, nullptr);
-    if (rc)
-        return rc;
-    return search_step_end(S, nullptr, n_active);
-}
-
-int search_result(tcse_search* S, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
-    tcse_ctx* ctx = S->ctx;
-    CU(cudaSetDevice(ctx->device));
-    uint64_t steps = 0, replayed = 0, wops = 0;
-    for (int s = 0; s < S->n_systems; ++s) {
-        const IncState& I = S->hinc[size_t(s)];
-        IncState fin;
-        CU(cudaMemcpyAsync(&fin, S->pool[size_t(s)].inc.p, sizeof fin, cudaMemcpyDeviceToHost, ctx->stream));
-        std::vector<u32> k(size_t(std::max(I.len, 1)));
-        if (best) {
-            if (I.len > best[s].cap)
-                return fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < %d", best[s].cap, I.len);
-            CU(cudaMemcpyAsync(k.data(), S->pool[size_t(s)].inc_keys.p, 4 * size_t(I.len), cudaMemcpyDeviceToHost,
-                               ctx->stream));
-        }
-        CU(cudaStreamSynchronize(ctx->stream));
-        if (best) {
-            for (int t = 0; t < I.len; ++t)
-                best[s].subs[t] = key_pair(k[size_t(t)]);
-            best[s].n_subs = I.len;
-            best[s].cost = I.cost;
-            best[s].strategy = I.strategy;
-            best[s].seed = I.seed;
-            S->d2h += 4 * uint64_t(I.len);
-        }
-        if (iterations)
-            iterations[s] = S->iters[size_t(s)];
-        steps += fin.steps;
-        replayed += fin.replayed;
-        wops += fin.wops;
-    }
-    if (stats) {
-        std::memset(stats, 0, sizeof *stats);
-        stats->steps = steps;
-        stats->replayed = replayed;
-        stats->wops = wops;
-        stats->processes = S->processes;
-        stats->launches = S->launches;
-        stats->iterations = S->iteration;
-        stats->retries = S->retries;
-        stats->kernel_ms = S->kernel_ms;
-        stats->step_ms = S->step_ms;
-        stats->exchange_ms = S->exchange_ms;
-        stats->h2d_bytes = S->h2d;
-        stats->d2h_bytes = S->d2h;
-        stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - S->t0).count();
-    }
-    return TCSE_OK;
-}
-
-}  // namespace
+#include "session.inc"
 
 extern "C" {
-
-int tcse_microbench_wordops_impl(int device, double* gops);
-
-int tcse_microbench_wordops(tcse_ctx* ctx, double* gops) {
-    if (!ctx || !gops)
-        return fail(TCSE_EINVAL, "tcse_microbench_wordops: bad argument");
-    const int rc = tcse_microbench_wordops_impl(ctx->device, gops);
-    return rc ? fail(rc, "microbenchmark failed") : TCSE_OK;
-}
-
-int tcse_search_create(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems, const tcse_search_config* cfg,
-                       const uint64_t* salts, tcse_iter_cb cb, void* user, tcse_search** out) {
-    if (!out)
-        return fail(TCSE_EINVAL, "tcse_search_create: null output");
-    *out = nullptr;
-    auto* S = new tcse_search;
-    const int rc = search_init(S, ctx, n_systems, systems, cfg, salts, cb, user);
-    if (rc) {
-        delete S;
-        return rc;
-    }
-    *out = S;
-    return TCSE_OK;
-}
-
-int tcse_search_step(tcse_search* S, int32_t* n_active) {
-    if (!S || !n_active)
-        return fail(TCSE_EINVAL, "tcse_search_step: bad argument");
-    return search_step(S, n_active);
-}
-
-int tcse_search_result(tcse_search* S, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
-    if (!S)
-        return fail(TCSE_EINVAL, "tcse_search_result: bad argument");
-    return search_result(S, best, iterations, stats);
-}
-
-size_t tcse_search_payload_bytes(tcse_search* S) { return S ? 4 * size_t(S->words_total) : 0; }
-
-int tcse_search_step_begin(tcse_search* S, void* send_dev) {
-    if (!S)
-        return fail(TCSE_EINVAL, "tcse_search_step_begin: bad argument");
-    return search_step_begin(S, send_dev);
-}
-
-int tcse_search_step_end(tcse_search* S, const void* recv_dev, int32_t* n_active) {
-    if (!S || !n_active)
-        return fail(TCSE_EINVAL, "tcse_search_step_end: bad argument");
-    return search_step_end(S, recv_dev, n_active);
-}
-
-void tcse_search_destroy(tcse_search* S) {
-    if (S) {
-        cudaSetDevice(S->ctx->device);
-        delete S;
-    }
-}
-
-int tcse_optimize_systems(tcse_ctx* ctx, int32_t n_systems, const tcse_system* systems,
-                          const tcse_search_config* cfg, const uint64_t* salts, tcse_iter_cb cb,
-                          void* user, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
-    if (!best)
-        return fail(TCSE_EINVAL, "optimize_systems: null result");
-    tcse_search* S = nullptr;
-    int rc = tcse_search_create(ctx, n_systems, systems, cfg, salts, cb, user, &S);
-    if (rc)
-        return rc;
-    for (int s = 0; s < n_systems; ++s)
-        if (best[s].cap < S->dev[size_t(s)].h.naive) {
-            rc = fail(TCSE_ECAPACITY, "optimize_system: record capacity %d < naive cost %d", best[s].cap,
-                      S->dev[size_t(s)].h.naive);
-            tcse_search_destroy(S);
-            return rc;
-        }
-    int32_t left = 1;
-    while (left > 0 && rc == TCSE_OK)
-        rc = search_step(S, &left);
-    if (rc == TCSE_OK)
-        rc = search_result(S, best, iterations, stats);
-    tcse_search_destroy(S);
-    return rc;
-}
-
-int tcse_optimize_system(tcse_ctx* ctx, const tcse_system* sys, const tcse_search_config* cfg, uint64_t stream_salt,
-                         tcse_iter_cb cb, void* user, tcse_record* best, int32_t* iterations, tcse_stats* stats) {
-    return tcse_optimize_systems(ctx, 1, sys, cfg, &stream_salt, cb, user, best, iterations, stats);
-}
 
 // replay_prefix + total_cost + expand_and_verify (linear_system.hpp:193-258)
 int tcse_verify_record(const tcse_system* sys, const tcse_pair* subs, int32_t n_subs, int32_t* cost_out) {

@@ -38,6 +38,42 @@ enum Mode : int32_t {
 // (the session re-runs the iteration at full capacity; never user-visible)
 constexpr int kErrCandOverflow = -100;
 
+// Device-resident loop state of one system (optimize_system's loop variables,
+// parallel_search.hpp:226-271): the incumbent, the iteration counter, patience
+// and the active flag live in HBM and are advanced by the barrier kernel, so
+// iterations run back to back without the host (CUDA graph replays); the host
+// reads this struct after a batch.
+struct IncState {
+    int32_t have;
+    int32_t cost;
+    int32_t len;
+    int32_t strategy;
+    u64 seed;
+    int32_t improved;   // set by the last barrier
+    int32_t best_p;     // global id of the iteration's best process
+    int32_t best_cost;
+    int32_t iteration;  // iterations completed
+    int32_t active;     // 1 while searching (cleared by patience / max_iterations)
+    int32_t unchanged;  // iterations without improvement (patience counter)
+    u64 steps;          // accumulated selected substitutions
+    u64 replayed;
+    u64 wops;           // accumulated algorithmic word-ops
+    u64 steps_by_strategy[8];  // selected substitutions per StrategyKind of the process
+};
+
+// Device clock of a session (%globaltimer, ns): per launch group the first
+// search block's start and the last one's end in the current iteration, the
+// exchange start, and the accumulated spans (graph replays included).
+struct LoopClock {
+    u64 gstart[kMaxSys];
+    u64 gend[kMaxSys];
+    u64 xstart;
+    u64 group_ns[kMaxSys];
+    u64 search_ns;    // union of the iteration's search-group spans
+    u64 exchange_ns;  // pack -> end of the barrier kernels
+    u64 iterations;   // iterations the clock saw
+};
+
 struct SysDesc {
     // problem (base state, shared read-only by every block of the system)
     int32_t n_x, n_e, naive;
@@ -76,6 +112,9 @@ struct SysDesc {
     const u8* reinit;     // [n_local] or null (search mode)
     const u32* inc_keys;  // incumbent record (reinit prefix source)
     int32_t inc_len;
+    // session: iteration, incumbent length and the active flag come from the
+    // device loop state instead of iteration / inc_len (null: host-driven)
+    const IncState* loop;
     const u32* prefix;  // fixed prefix (run / dump modes)
     int32_t prefix_len;
 
@@ -102,8 +141,8 @@ struct SysDesc {
 
 // per-process configuration handed from the prep kernel to the search kernel
 struct SlotRec {
-    int32_t strategy;
-    int32_t reinit;  // restart from an incumbent prefix
+    int32_t strategy;  // -1: skip (system inactive or the launch hit an error)
+    int32_t reinit;    // > 0: restart from a prefix of the incumbent, whose length this is
     int32_t rng;     // the process draws from its mt19937_64 stream
     int32_t pad;
     double alpha, beta, p_greedy;
@@ -120,23 +159,9 @@ struct LaunchDesc {
     int32_t* hist;   // [kMaxSys][kHistStride] (strategy, work class) histogram + placement cursors
     const SysDesc* table;  // > kMaxSys systems (flip mode): device table, blocks contiguous per system
     int32_t table_n;
+    int32_t group;         // launch group index (clock stamps)
+    LoopClock* clock;      // or null
     SysDesc sys[kMaxSys];
-};
-
-// per-system state of the iteration reduce (K2)
-struct IncState {
-    int32_t have;
-    int32_t cost;
-    int32_t len;
-    int32_t strategy;
-    u64 seed;
-    int32_t improved;  // set by the last reduce
-    int32_t best_p;    // global id of the iteration's best process
-    int32_t best_cost;
-    int32_t reserved;
-    u64 steps;         // accumulated selected substitutions
-    u64 replayed;
-    u64 wops;          // accumulated algorithmic word-ops
 };
 
 // Exchange payload of one rank for one system (int32 words, fixed size):
@@ -144,9 +169,14 @@ struct IncState {
 //   n_max + 0             1 if the rank ran at least one process
 //   n_max + 1             global id of the rank's best process (min cost, lowest id)
 //   n_max + 2, 3, 4..5    its record length, strategy, seed (lo, hi)
-//   n_max + 6 ..          its record (u32 pair keys), sub_cap entries
+//   n_max + 6             the rank's launch error (0 = none): every rank then
+//                         skips the barrier and reports it (a capacity retry
+//                         re-runs the iteration on every rank)
+//   n_max + kHdr ..       its record (u32 pair keys), sub_cap entries
 // With world = 1 the gathered buffer is this payload itself, so one code
 // path serves every world size.
+constexpr int kHdr = 8;
+
 struct XchgDesc {
     int32_t n, world, n_max, sys_off, words_total;  // layout (words)
     int32_t n_local, p0, sub_cap;
@@ -164,10 +194,20 @@ struct XchgDesc {
     u8* reinit_next;  // [n]
     double fraction;
     int32_t hist_n;
+    int32_t patience, max_iterations;
+    // barrier scratch: nblk tally blocks over the n gathered costs
+    int32_t nblk;
+    u64* part_min;     // [nblk] (cost << 32 | p)
+    int32_t* part_hist;  // [nblk][hist_n] cost histograms
+    u64* part_sums;    // [nblk][3 + 8]: steps, replayed, word-ops, steps per strategy
+    int32_t* part_off;   // [nblk] ties at the threshold cost before the block
+    int32_t* sel;        // [4]: threshold cost, ties to take, count, improved-rank
 };
 
 struct XchgLaunch {
     int32_t nsys;
+    int32_t* err;  // the launch error word of this rank (shared with the search launches)
+    LoopClock* clock;
     XchgDesc x[kMaxSys];
 };
 

@@ -114,6 +114,12 @@ __device__ unsigned long long g_gi_stats[8];
 __device__ __forceinline__ double __int_as_double_lo(int v) { return __hiloint2double(0, v); }
 __device__ __forceinline__ int __double_lo_as_int(double d) { return __double2loint(d); }
 
+__device__ __forceinline__ u64 globaltimer() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <typename T>
 __device__ __forceinline__ T* sp(u32 off) {
     return reinterpret_cast<T*>(g_smem + off);
@@ -468,11 +474,11 @@ struct Slot {
 
 // assign_strategies (parallel_search.hpp:183-205) for global process p: the
 // first five outputs of mt19937_64(mix_seed{master, salt, iteration, p})
-__device__ __noinline__ void derive_slot(const SysDesc& sd, u64 p, Slot* out) {
+__device__ __noinline__ void derive_slot(const SysDesc& sd, int iteration, u64 p, Slot* out) {
     u64 h = 0x5851f42d4c957f2dULL;
     h = splitmix64(h ^ sd.master_seed);
     h = splitmix64(h ^ sd.salt);
-    h = splitmix64(h ^ u64(int64_t(sd.iteration)));
+    h = splitmix64(h ^ u64(int64_t(iteration)));
     h = splitmix64(h ^ p);
     u64 x = h;
     const u64 l0 = x;
@@ -509,7 +515,7 @@ __device__ __noinline__ void derive_slot(const SysDesc& sd, u64 p, Slot* out) {
     if (sd.forced >= 0) {
         out->strategy = sd.forced;
         out->seed = o3;
-    } else if (sd.iteration == 1 && p == 0) {
+    } else if (iteration == 1 && p == 0) {
         out->strategy = TCSE_GREEDY;
         out->seed = o3;
     } else {
@@ -1905,6 +1911,10 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     }
     __syncthreads();
     const int strategy = s_slot.strategy;
+    if (strategy < 0)  // converged system or failed launch (prep_kernel)
+        return;
+    if (tid == 0 && L.clock)
+        atomicMin(&L.clock->gstart[L.group], globaltimer());
     const int reinit = s_slot.reinit;
     const double alpha = s_slot.alpha, beta = s_slot.beta, p_greedy = s_slot.p_greedy;
     const double* s_mix = s_slot.mix;
@@ -1938,7 +1948,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     const u32* pre = nullptr;
     int n_pre = 0;
     if (reinit) {
-        const u64 k_max = u64(3 * sd.inc_len / 4);
+        const u64 k_max = u64(3 * reinit / 4);  // reinit = incumbent length
         n_pre = int(1 + pr.nd(k_max));
         pre = sd.inc_keys;
     } else if (sd.mode != kModeSearch && sd.prefix_len > 0) {
@@ -2053,6 +2063,8 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         sd.out_seed[lp] = s_slot.seed;
         if (sd.out_wops)
             sd.out_wops[lp] = wops;
+        if (L.clock)
+            atomicMax(&L.clock->gend[L.group], globaltimer());
     }
 }
 
@@ -2076,10 +2088,23 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     const int lp = b - sd.block_begin;
     if (lp >= sd.n_local)
         return;
+    // the iteration and the incumbent length: from the device loop state in a
+    // session (graph replays need no host parameters), else from the descriptor
+    int iteration = sd.iteration, inc_len = sd.inc_len;
+    if (sd.loop) {
+        if (!sd.loop->active || *sd.err != 0) {  // converged system, or the launch already failed
+            L.slots[b].strategy = -1;
+            if (L.hist)
+                atomicAdd(&L.hist[s * kHistStride + 7], 1);  // placed last (strategy slot 7 is unused)
+            return;
+        }
+        iteration = sd.loop->iteration + 1;
+        inc_len = sd.loop->len;
+    }
     SlotRec r;
     Slot sl;
     if (sd.mode == kModeSearch) {
-        derive_slot(sd, u64(sd.p0) + u64(lp) * u64(max(sd.p_stride, 1)), &sl);
+        derive_slot(sd, iteration, u64(sd.p0) + u64(lp) * u64(max(sd.p_stride, 1)), &sl);
         for (int k = 0; k < 4; ++k)
             r.mix[k] = sd.mix[k];
     } else if (sd.mode == kModeRun) {
@@ -2098,13 +2123,13 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
         for (int k = 0; k < 4; ++k)
             r.mix[k] = 0.0;
     }
-    const int reinit = (sd.mode == kModeSearch && sd.reinit && sd.reinit[lp]) ? 1 : 0;
+    const int reinit = (sd.mode == kModeSearch && sd.reinit && sd.reinit[lp] && inc_len >= 2) ? 1 : 0;
     const int st = sl.strategy;
     const bool rng = reinit || st == TCSE_GREEDY_ALTERNATIVE || st == TCSE_WEIGHTED_RANDOM ||
                      st == TCSE_GREEDY_RANDOM || st == TCSE_MIXED ||
                      (st == TCSE_GREEDY_INTERSECTIONS && sl.alpha != 0.0);
     r.strategy = st;
-    r.reinit = reinit;
+    r.reinit = reinit ? inc_len : 0;
     r.rng = rng ? 1 : 0;
     r.pad = 0;
     r.alpha = sl.alpha;
@@ -2131,8 +2156,8 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
         if (reinit) {
             const u64* m0 = L.rng + size_t(b) * 312;
             const u64 x = mt_temper(mt_mix(m0[0], m0[1], m0[156]));
-            const u64 n_pre = 1 + __umul64hi(x, u64(3 * sd.inc_len / 4));
-            cls = 1 + min(3, int(4 * n_pre / u64(sd.inc_len + 1)));
+            const u64 n_pre = 1 + __umul64hi(x, u64(3 * inc_len / 4));
+            cls = 1 + min(3, int(4 * n_pre / u64(inc_len + 1)));
         }
         L.slots[b].pad = cls;
         atomicAdd(&L.hist[s * kHistStride + st + 8 * cls], 1);
@@ -2153,14 +2178,15 @@ __global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ Laun
     const SysDesc& sd = L.sys[s];
     if (b - sd.block_begin >= sd.n_local)
         return;
-    const int order[7] = {TCSE_GREEDY_POTENTIAL, TCSE_GREEDY_INTERSECTIONS, TCSE_MIXED, TCSE_GREEDY_RANDOM,
-                          TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY};
+    const int order[8] = {TCSE_GREEDY_POTENTIAL, TCSE_GREEDY_INTERSECTIONS, TCSE_MIXED, TCSE_GREEDY_RANDOM,
+                          TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY, 7};
     // within a strategy, fresh processes before reinit ones (which replay part
-    // of the incumbent instead of selecting: shorter)
-    const int st = L.slots[b].strategy, cls = L.slots[b].pad;
+    // of the incumbent instead of selecting: shorter); skipped blocks (slot 7) last
+    const int st0 = L.slots[b].strategy;
+    const int st = st0 < 0 ? 7 : st0, cls = st0 < 0 ? 0 : L.slots[b].pad;
     const int* h = L.hist + s * kHistStride;
     int base = sd.block_begin;
-    for (int k = 0; k < 7 && order[k] != st; ++k)
+    for (int k = 0; k < 8 && order[k] != st; ++k)
 #pragma unroll
         for (int c = 0; c < kWorkClasses; ++c)
             base += h[order[k] + 8 * c];
@@ -2170,18 +2196,69 @@ __global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ Laun
 }
 
 // ----------------------------------------------------------------- K2
+//
+// The iteration barrier (parallel_search.hpp:237-270) as four short kernels
+// on the launch stream, all reading only device state so a whole iteration
+// can be replayed from a CUDA graph:
+//   pack   — this rank's payload: its slice of costs, its best record, its
+//            launch error;
+//   (the payloads are all-gathered here when world > 1: NCCL on the stream)
+//   tally  — nblk blocks per system over the n gathered costs: partial argmin,
+//            per-block cost histograms, this rank's step / word-op sums;
+//   barrier— one block per system: global argmin by (cost, id), strict
+//            improvement, incumbent record copy, patience and max_iterations
+//            (the loop variables of optimize_system), the reinit threshold
+//            cost and the per-block tie offsets for pick_reinit (149-163);
+//   flags  — nblk blocks per system: the next iteration's reinit flags.
+// A launch error on any rank (device capacity, replay) skips the barrier on
+// every rank, so the host re-runs or reports the same iteration everywhere.
 
 __device__ __forceinline__ int part_of(int n, int world, int r) { return int((long long)n * r / world); }
 
-constexpr int kRedNT = 1024;
+constexpr int kRedNT = 1024;  // pack / barrier block
+constexpr int kTallyNT = 256;  // tally / flags block
+constexpr int kTallyPer = 2048;  // gathered costs per tally block
+
+// owner rank of global process p (contiguous partition)
+__device__ __forceinline__ int owner_of(int n, int world, int p) {
+    int r = int((long long)p * world / n);
+    while (r + 1 < world && part_of(n, world, r + 1) <= p)
+        ++r;
+    while (r > 0 && part_of(n, world, r) > p)
+        --r;
+    return r;
+}
+
+__device__ __forceinline__ int gathered_cost(const XchgDesc& X, int p) {
+    const int r = owner_of(X.n, X.world, p);
+    return X.recv[size_t(r) * size_t(X.words_total) + size_t(X.sys_off) + size_t(p - part_of(X.n, X.world, r))];
+}
+
+// first launch error among the gathered payloads (0 = none)
+__device__ __forceinline__ int gathered_error(const XchgDesc& X) {
+    int e = 0;
+    for (int r = 0; r < X.world && e == 0; ++r)
+        e = X.recv[size_t(r) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + 6];
+    return e;
+}
 
 // K2a: this rank's payload (local argmin + record copy), one block per system
 __global__ void __launch_bounds__(kRedNT) pack_kernel(const __grid_constant__ XchgLaunch XL) {
     const XchgDesc& X = XL.x[blockIdx.x];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (blockIdx.x == 0 && tid == 0 && XL.clock)
+        XL.clock->xstart = globaltimer();
+    if (!X.inc->active)
+        return;  // every rank agrees (identical barriers)
     __shared__ u64 s_min[32];
     __shared__ int s_bp;
     int32_t* out = X.send + X.sys_off;
+    const int err = *XL.err;
+    if (err != 0) {  // only the error travels
+        if (tid == 0)
+            out[X.n_max + 6] = err;
+        return;
+    }
     u64 best = ~0ULL;
     for (int t = tid; t < X.n_local; t += kRedNT) {
         const int32_t c = X.cost[t];
@@ -2207,84 +2284,123 @@ __global__ void __launch_bounds__(kRedNT) pack_kernel(const __grid_constant__ Xc
         const u64 sd = t >= 0 ? X.seed[t] : 0;
         h[4] = int32_t(u32(sd));
         h[5] = int32_t(u32(sd >> 32));
+        h[6] = 0;
+        h[7] = 0;
         s_bp = t;
     }
     __syncthreads();
     const int t = s_bp;
     if (t >= 0) {
         const int L = X.len[t];
-        int32_t* rec = out + X.n_max + 6;
+        int32_t* rec = out + X.n_max + kHdr;
         for (int e = tid; e < L; e += kRedNT)
             rec[e] = int32_t(X.subs[size_t(t) * size_t(X.sub_cap) + size_t(e)]);
     }
 }
 
-// K2b: the iteration barrier over the gathered payloads
-__global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ XchgLaunch XL) {
+// K2b: per-block partials over the gathered costs (grid: nblk x nsys)
+__global__ void __launch_bounds__(kTallyNT) tally_kernel(const __grid_constant__ XchgLaunch XL) {
     extern __shared__ int hist[];
-    const XchgDesc& X = XL.x[blockIdx.x];
+    const XchgDesc& X = XL.x[blockIdx.y];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __shared__ u64 s_min[32];
-    __shared__ u64 s_sum[32];
-    __shared__ u64 s_rep[32];
-    __shared__ u64 s_wop[32];
-    __shared__ u32 s_red[34];
-    __shared__ int s_thr[3];
-    const int n = X.n, world = X.world;
-    auto gcost = [&](int p) -> int {
-        int r = int((long long)p * world / n);  // owner rank guess, corrected below
-        while (r + 1 < world && part_of(n, world, r + 1) <= p)
-            ++r;
-        while (r > 0 && part_of(n, world, r) > p)
-            --r;
-        return X.recv[size_t(r) * size_t(X.words_total) + size_t(X.sys_off) + size_t(p - part_of(n, world, r))];
-    };
-    // argmin over (cost, global process id) — lowest index wins ties (255-260)
-    u64 best = ~0ULL;
-    for (int p = tid; p < n; p += kRedNT)
-        best = min(best, (u64(u32(gcost(p))) << 32) | u64(u32(p)));
-    u64 steps = 0, replayed = 0, wops = 0;
-    for (int t = tid; t < X.n_local; t += kRedNT) {
-        steps += u64(X.own[t]);
-        replayed += u64(X.len[t] - X.own[t]);
-        wops += X.wops[t];
+    if (!X.inc->active || *XL.err != 0)
+        return;
+    const int ge = gathered_error(X);
+    if (ge != 0) {  // another rank failed: skip the barrier everywhere
+        if (blockIdx.x == 0 && tid == 0)
+            atomicCAS(XL.err, 0, ge);
+        return;
     }
+    const int blk = blockIdx.x;
+    for (int v = tid; v < X.hist_n; v += kTallyNT)
+        hist[v] = 0;
+    __syncthreads();
+    const int p0 = blk * kTallyPer, p1 = min(X.n, p0 + kTallyPer);
+    u64 best = ~0ULL;
+    for (int p = p0 + tid; p < p1; p += kTallyNT) {
+        const int c = gathered_cost(X, p);
+        best = min(best, (u64(u32(c)) << 32) | u64(u32(p)));
+        atomicAdd(&hist[min(max(c, 0), X.hist_n - 1)], 1);
+    }
+    // this rank's own processes, same block split over the local slice
+    constexpr int kS = 3 + 8;
+    u64 sums[kS];
+#pragma unroll
+    for (int k = 0; k < kS; ++k)
+        sums[k] = 0;
+    const int lper = (X.n_local + gridDim.x - 1) / gridDim.x;
+    const int l0 = min(X.n_local, blk * lper), l1 = min(X.n_local, l0 + lper);
+    for (int t = l0 + tid; t < l1; t += kTallyNT) {
+        const u64 own = u64(X.own[t]);
+        sums[0] += own;
+        sums[1] += u64(X.len[t] - X.own[t]);
+        sums[2] += X.wops[t];
+        const int st = X.strat[t];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            sums[3 + k] += st == k ? own : 0;
+    }
+    __shared__ u64 s_red[kTallyNT / 32][kS + 1];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         best = min(best, __shfl_down_sync(FULLMASK, best, o));
-        steps += __shfl_down_sync(FULLMASK, steps, o);
-        replayed += __shfl_down_sync(FULLMASK, replayed, o);
-        wops += __shfl_down_sync(FULLMASK, wops, o);
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            sums[k] += __shfl_down_sync(FULLMASK, sums[k], o);
     }
     if (lane == 0) {
-        s_min[warp] = best;
-        s_sum[warp] = steps;
-        s_rep[warp] = replayed;
-        s_wop[warp] = wops;
+        s_red[warp][0] = best;
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            s_red[warp][1 + k] = sums[k];
     }
-    for (int v = tid; v < X.hist_n; v += kRedNT)
-        hist[v] = 0;
     __syncthreads();
+    if (tid < kS + 1) {
+        u64 v = tid == 0 ? ~0ULL : 0;
+        for (int w = 0; w < kTallyNT / 32; ++w)
+            v = tid == 0 ? min(v, s_red[w][0]) : v + s_red[w][tid];
+        if (tid == 0)
+            X.part_min[blk] = v;
+        else
+            X.part_sums[size_t(blk) * kS + size_t(tid - 1)] = v;
+    }
+    for (int v = tid; v < X.hist_n; v += kTallyNT)
+        X.part_hist[size_t(blk) * size_t(X.hist_n) + size_t(v)] = hist[v];
+}
+
+// K2c: the barrier itself, one block per system
+__global__ void __launch_bounds__(kRedNT) barrier_kernel(const __grid_constant__ XchgLaunch XL) {
+    extern __shared__ int hist[];
+    const XchgDesc& X = XL.x[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!X.inc->active || *XL.err != 0)
+        return;
+    __shared__ int s_thr[4];
+    const int n = X.n, world = X.world, nb = X.nblk;
     if (tid == 0) {
-        u64 b = s_min[0], st = 0, rp = 0, wo = 0;
-        for (int w = 0; w < kRedNT / 32; ++w) {
-            b = min(b, s_min[w]);
-            st += s_sum[w];
-            rp += s_rep[w];
-            wo += s_wop[w];
+        u64 b = ~0ULL;
+        constexpr int kS = 3 + 8;
+        u64 sums[kS];
+        for (int k = 0; k < kS; ++k)
+            sums[k] = 0;
+        for (int k = 0; k < nb; ++k) {
+            b = min(b, X.part_min[k]);
+            for (int j = 0; j < kS; ++j)
+                sums[j] += X.part_sums[size_t(k) * kS + size_t(j)];
         }
+        // argmin over (cost, global process id): lowest index wins ties (255-260)
         const int bp = int(b & 0xffffffffu);
         const int bc = int(b >> 32);
-        int rb = 0;  // the rank that owns bp carries its record
-        while (rb + 1 < world && part_of(n, world, rb + 1) <= bp)
-            ++rb;
+        const int rb = owner_of(n, world, bp);  // the rank that owns bp carries its record
         const int32_t* h = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max);
         IncState* inc = X.inc;
         inc->best_p = bp;
         inc->best_cost = bc;
-        inc->steps += st;
-        inc->replayed += rp;
-        inc->wops += wo;
+        inc->steps += sums[0];
+        inc->replayed += sums[1];
+        inc->wops += sums[2];
+        for (int k = 0; k < 8; ++k)
+            inc->steps_by_strategy[k] += sums[3 + k];
         if (!inc->have || bc < inc->cost) {  // strictly better (261-266)
             inc->have = 1;
             inc->cost = bc;
@@ -2292,9 +2408,15 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
             inc->strategy = h[3];
             inc->seed = u64(u32(h[4])) | (u64(u32(h[5])) << 32);
             inc->improved = 1;
+            inc->unchanged = 0;
         } else {
             inc->improved = 0;
+            inc->unchanged += 1;
         }
+        // the loop condition of optimize_system (268-270) + the stop knob
+        inc->iteration += 1;
+        if (inc->unchanged >= X.patience || (X.max_iterations > 0 && inc->iteration >= X.max_iterations))
+            inc->active = 0;
         s_thr[0] = inc->improved ? rb : -1;
         s_thr[1] = inc->len;
     }
@@ -2302,65 +2424,143 @@ __global__ void __launch_bounds__(kRedNT) reduce_kernel(const __grid_constant__ 
     const int rb = s_thr[0];
     const int inc_len = s_thr[1];
     if (rb >= 0) {
-        const int32_t* rec = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + 6;
+        const int32_t* rec = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + kHdr;
         for (int t = tid; t < inc_len; t += kRedNT)
             X.inc_keys[t] = u32(rec[t]);
     }
     // pick_reinit (149-163) for the next iteration, only if the incumbent can
-    // share a prefix (235-237)
+    // share a prefix (235-237): histogram of all costs -> threshold cost c*
     const long long want = llround(__dmul_rn(X.fraction, double(n)));
     const int count = inc_len >= 2 ? int(min(want, (long long)n)) : 0;
     if (count <= 0) {
-        for (int p = tid; p < n; p += kRedNT)
+        if (tid == 0)
+            X.sel[2] = 0;
+        return;
+    }
+    for (int v = tid; v < X.hist_n; v += kRedNT) {
+        int acc = 0;
+        for (int k = 0; k < nb; ++k)
+            acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(v)];
+        hist[v] = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // threshold c*: all costs > c* are chosen, plus the first `need`
+        // processes (by index) with cost == c* (stable order, 158-160);
+        // one warp scans the histogram from the top, 32 costs at a time
+        int acc = 0, cstar = 0, need = 0;
+        for (int top = X.hist_n - 1; top >= 0; top -= 32) {
+            const int c = top - lane;
+            const int hc = c >= 0 ? hist[c] : 0;
+            int incl = hc;  // inclusive scan from the top cost down
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULLMASK, incl, o);
+                if (lane >= o)
+                    incl += y;
+            }
+            const unsigned hit = __ballot_sync(FULLMASK, c >= 0 && acc + incl >= count);
+            if (hit) {
+                const int l = __ffs(hit) - 1;
+                const int il = __shfl_sync(FULLMASK, incl, l), hl = __shfl_sync(FULLMASK, hc, l);
+                cstar = top - l;
+                need = count - (acc + il - hl);
+                break;
+            }
+            acc += __shfl_sync(FULLMASK, incl, 31);
+        }
+        if (lane == 0) {
+            s_thr[2] = cstar;
+            s_thr[3] = need;
+        }
+    }
+    __syncthreads();
+    const int cstar = s_thr[2], need = s_thr[3];
+    if (tid == 0) {
+        X.sel[0] = cstar;
+        X.sel[1] = need;
+        X.sel[2] = count;
+        int acc = 0;  // ties at c* before each tally block (index order)
+        for (int k = 0; k < nb; ++k) {
+            X.part_off[k] = acc;
+            acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1))];
+        }
+    }
+}
+
+// K2d: the next iteration's reinit flags (grid: nblk x nsys)
+__global__ void __launch_bounds__(kTallyNT) flags_kernel(const __grid_constant__ XchgLaunch XL) {
+    const XchgDesc& X = XL.x[blockIdx.y];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && XL.clock) {
+        // the iteration's device clock (once per iteration, before any exit)
+        LoopClock* k = XL.clock;
+        u64 lo = ~0ULL, hi = 0;
+        for (int g = 0; g < kMaxSys; ++g) {
+            if (k->gstart[g] != ~0ULL && k->gend[g] > k->gstart[g]) {
+                k->group_ns[g] += k->gend[g] - k->gstart[g];
+                lo = min(lo, k->gstart[g]);
+                hi = max(hi, k->gend[g]);
+            }
+            k->gstart[g] = ~0ULL;
+            k->gend[g] = 0;
+        }
+        if (hi > lo) {
+            k->search_ns += hi - lo;
+            k->iterations += 1;
+        }
+        const u64 now = globaltimer();
+        if (k->xstart != 0 && now > k->xstart)
+            k->exchange_ns += now - k->xstart;
+        k->xstart = 0;
+    }
+    // a system that just converged keeps its last flags (never read again)
+    if (!X.inc->active || *XL.err != 0)
+        return;
+    const int n = X.n;
+    const int p0 = blockIdx.x * kTallyPer, p1 = min(n, p0 + kTallyPer);
+    if (X.sel[2] <= 0) {
+        for (int p = p0 + tid; p < p1; p += kTallyNT)
             X.reinit_next[p] = 0;
         return;
     }
-    for (int p = tid; p < n; p += kRedNT)
-        atomicAdd(&hist[min(max(gcost(p), 0), X.hist_n - 1)], 1);
-    __syncthreads();
-    if (tid == 0) {
-        // threshold cost c*: all costs > c* are chosen, plus the first `need`
-        // processes (by index) with cost == c* (stable order, 158-160)
-        int acc = 0, cstar = 0, need = 0;
-        for (int c = X.hist_n - 1; c >= 0; --c) {
-            if (acc + hist[c] >= count) {
-                cstar = c;
-                need = count - acc;
-                break;
-            }
-            acc += hist[c];
-        }
-        s_thr[0] = cstar;
-        s_thr[1] = need;
+    const int cstar = X.sel[0], need = X.sel[1];
+    // each thread a contiguous run of the block's range; ordered tie scan
+    constexpr int kPer = kTallyPer / kTallyNT;
+    const int e0 = min(p1, p0 + tid * kPer), e1 = min(p1, e0 + kPer);
+    int cs[kPer];
+    int local = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        cs[k] = e0 + k < e1 ? gathered_cost(X, e0 + k) : -1;
+        local += cs[k] == cstar ? 1 : 0;
     }
-    __syncthreads();
-    const int cstar = s_thr[0], need = s_thr[1];
-    const int E = (n + kRedNT - 1) / kRedNT;
-    const int e0 = min(n, tid * E), e1 = min(n, e0 + E);
-    u32 local = 0;
-    for (int e = e0; e < e1; ++e)
-        local += gcost(e) == cstar ? 1u : 0u;
-    const u32 inc_ = warp_incl_scan(local, lane);
+    __shared__ int s_w[kTallyNT / 32];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULLMASK, incl, o);
+        if (lane >= o)
+            incl += y;
+    }
     if (lane == 31)
-        s_red[warp] = inc_;
+        s_w[warp] = incl;
     __syncthreads();
-    if (warp == 0) {
-        const u32 w = s_red[lane];
-        const u32 wi = warp_incl_scan(w, lane);
-        s_red[lane] = wi - w;
-    }
-    __syncthreads();
-    u32 ex = s_red[warp] + inc_ - local;
-    for (int e = e0; e < e1; ++e) {
-        const int c = gcost(e);
+    int ex = X.part_off[blockIdx.x] + incl - local;
+    for (int w = 0; w < warp; ++w)
+        ex += s_w[w];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        if (e0 + k >= e1)
+            break;
         u8 f = 0;
-        if (c > cstar) {
+        if (cs[k] > cstar) {
             f = 1;
-        } else if (c == cstar) {
-            f = ex < u32(need) ? 1 : 0;
+        } else if (cs[k] == cstar) {
+            f = ex < need ? 1 : 0;
             ++ex;
         }
-        X.reinit_next[e] = f;
+        X.reinit_next[e0 + k] = f;
     }
 }
 
@@ -2422,12 +2622,20 @@ cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+int barrier_blocks(int n) { return (n + kTallyPer - 1) / kTallyPer; }
+
+// tally -> barrier -> flags (the exchange, if any, ran before on the stream)
 cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st) {
     const int smem = hist_n * int(sizeof(int));
-    cudaError_t e = cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int nb = XL.x[0].nblk;
+    cudaError_t e = cudaFuncSetAttribute(tally_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(barrier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
-    reduce_kernel<<<XL.nsys, kRedNT, smem, st>>>(XL);
+    tally_kernel<<<dim3(nb, XL.nsys), kTallyNT, smem, st>>>(XL);
+    barrier_kernel<<<XL.nsys, kRedNT, smem, st>>>(XL);
+    flags_kernel<<<dim3(nb, XL.nsys), kTallyNT, 0, st>>>(XL);
     return cudaGetLastError();
 }
 

@@ -139,10 +139,13 @@ def parse_report(text):
     for k in range(7):
         w = c.get("strategy_weights", {})
         weights[k] = float(w.get(STRATEGY_SHORT[k], w.get(STRATEGY_NAMES[k], 0.0)))
+    fm = c.get("flip_mode", {})  # config_from_json (io.hpp:190-196)
     cfg = SearchConfig(n_processes=c.get("n_processes", 0), strategy_weights=weights,
                        reinit_fraction=c.get("reinit_fraction", 0.4), patience=c.get("patience", 10),
                        master_seed=c.get("master_seed", 0),
-                       forced_strategy=_strategy_index(c["strategy"]) if c.get("strategy") else None)
+                       forced_strategy=_strategy_index(c["strategy"]) if c.get("strategy") else None,
+                       flip_enabled=bool(fm.get("enabled", False)), m_schemes=fm.get("m_schemes", 32),
+                       flips_min=fm.get("flips_min", 1), flips_max=fm.get("flips_max", 16))
     comps = []
     for key in "uvw":
         cj = j["components"][key]
@@ -152,11 +155,17 @@ def parse_report(text):
                 raise ValueError("report json: substitutions must be [i, j, sign] triples")
             subs.append(tuple(entry))
         rec = _Rec(subs, cj["cost"], _strategy_index(cj.get("strategy", "greedy")), cj.get("seed", 0))
-        comps.append(dict(record=rec, cost=cj["cost"], naive=cj["naive"], iterations=cj.get("iterations", 0)))
+        comp = dict(record=rec, cost=cj["cost"], naive=cj["naive"], iterations=cj.get("iterations", 0))
+        if "scheme_id" in cj:  # component_from_json (io.hpp:242)
+            comp["scheme_id"] = cj["scheme_id"]
+        comps.append(comp)
     rep = dict(scheme_digest=j["scheme_digest"], config=cfg, components=comps, total=j["total"],
                iterations=j["iterations"])
     if j.get("combined"):
         rep["combined"] = True
+    if "scheme" in j:  # the carried (flipped) scheme (io.hpp:285-286)
+        from .scheme import parse_scheme
+        rep["scheme"] = parse_scheme(json.dumps(j["scheme"]))
     return rep
 
 

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_loads_without_gpu_and_reports_abi():
     lib = T.lib()
-    assert lib.tcse_abi_version() == 1
+    assert lib.tcse_abi_version() == 2
     cfg = _abi.SearchConfig()
     lib.tcse_default_search_config(C.byref(cfg))
     assert list(cfg.strategy_weights) == [0.0, 4.0, 1.0, 2.0, 8.0, 0.1, 0.01]

@@ -103,3 +103,21 @@ def test_cli_reduce_reproduces_reference_files(tmp_path, name):
     assert out.returncode == 0, out.stderr
     assert rep.read_text() == r["json"]
     assert slp.read_text() == r["slp"]
+
+
+def test_flip_report_round_trip_and_combine():
+    """parse_report keeps flip_mode, per-component scheme_id and the carried
+    scheme (io.hpp:190-196, 242, 285-286): flip reports of the reference
+    round-trip byte-identically and combine like the reference's."""
+    with open(os.path.join(os.path.dirname(__file__), "golden", "flip_reports.json")) as f:
+        g = json.load(f)
+    reps = [T.parse_report(x) for x in g["reports"]]
+    for text, rep in zip(g["reports"], reps):
+        assert rep["config"]["flip_enabled"] is True
+        assert rep["scheme"]["r"] == 27 and all("scheme_id" in c for c in rep["components"])
+        assert T.report_to_json(rep) == text
+    a, b = g["combine_pair"]
+    assert T.report_to_json(T.combine_componentwise([reps[a], reps[b]])) == g["combined"]
+    if reps[0]["scheme_digest"] != reps[1]["scheme_digest"]:
+        with pytest.raises(ValueError, match="different schemes"):
+            T.combine_componentwise(reps)

@@ -5,7 +5,7 @@ proj/tools/terncse_cli.cpp, for the search path):
   tcse_cli.py verify  scheme.json
   tcse_cli.py reduce  scheme.json [--processes N] [--iterations-patience P] [--reinit-fraction F]
                       [--weights gi=8,ga=4,...] [--seed S] [--strategy NAME] [--config report.json]
-                      [--out-slp FILE] [--out-report FILE]
+                      [--flip-mode] [--flip-schemes M] [--out-slp FILE] [--out-report FILE]
   tcse_cli.py combine report.json... [--out-report FILE]
 
 Errors print one `error: ...` line and exit 1 (terncse_cli.cpp:215-218).
@@ -78,9 +78,14 @@ def cmd_reduce(args):
         if k is None:
             raise T.TcseError(-1, 'unknown strategy "%s"' % args.strategy)
         cfg["forced_strategy"] = k
-    rep = T.optimize_scheme(s, cfg)
+    if args.flip_mode:
+        cfg["flip_enabled"] = True
+    if args.flip_schemes is not None:
+        cfg["m_schemes"] = args.flip_schemes
+    # flip mode dispatches to optimize_with_flips (terncse_cli.cpp:85-86)
+    rep = T.optimize_with_flips(s, cfg) if cfg["flip_enabled"] else T.optimize_scheme(s, cfg)
     print("scheme: %dx%dx%d:%d digest: %s" % (s["m"], s["n"], s["p"], s["r"], rep["scheme_digest"]))
-    print_naive(s)
+    print_naive(rep.get("scheme") or s)
     c = [x["cost"] for x in rep["components"]]
     print("reduced: U=%d V=%d W=%d total=%d" % (c[0], c[1], c[2], rep["total"]))
     st = [T.STRATEGY_NAMES[x["record"].strategy] for x in rep["components"]]
@@ -92,7 +97,7 @@ def cmd_reduce(args):
             f.write(T.report_to_json(rep))
     if args.out_slp:
         with open(args.out_slp, "w") as f:
-            f.write(T.emit_slp(rep, s))
+            f.write(T.emit_slp(rep, rep.get("scheme") or s))
     return 0
 
 
@@ -124,6 +129,8 @@ def main(argv=None):
     r.add_argument("--weights")
     r.add_argument("--seed", type=int)
     r.add_argument("--strategy")
+    r.add_argument("--flip-mode", action="store_true")
+    r.add_argument("--flip-schemes", type=int)
     r.add_argument("--out-slp")
     r.add_argument("--out-report")
     c = sub.add_parser("combine")
