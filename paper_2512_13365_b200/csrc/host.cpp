@@ -256,6 +256,7 @@ struct tcse_ctx {
     ncclComm_t comm = nullptr;  // payload all-gather on `stream` (tcse_set_nccl / tcse_create_devices)
     bool own_comm = false;
     std::vector<tcse_ctx*> sub;  // multi-device context: rank r runs on sub[r]
+    std::shared_ptr<void> local_gather;  // test transport of a shared-device context (below)
     DBuf err;  // int32 err + err_pos
     DBuf slots, rng, perm, hist;  // prep_kernel -> search_kernel hand-off
     // launch groups beyond the first run on their own streams, forked from and
@@ -759,6 +760,60 @@ int tcse_set_nccl(tcse_ctx* ctx, const void* unique_id, int32_t rank, int32_t wo
     return TCSE_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// In-process all-gather between the rank threads of one context: the
+// transport of a shared-device context, which NCCL refuses (one rank per
+// GPU).  Only for TCSE_SHARED_DEVICES=1 test runs of the multi-device
+// orchestration on a single GPU; payloads go through host memory.
+struct LocalGather {
+    int world;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<std::vector<char>> slot;
+    int arrived = 0, phase = 0;
+    explicit LocalGather(int w) : world(w), slot(size_t(w)) {}
+    void barrier(std::unique_lock<std::mutex>& lk) {
+        const int ph = phase;
+        if (++arrived == world) {
+            arrived = 0;
+            ++phase;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return phase != ph; });
+        }
+    }
+};
+
+struct LocalRank {
+    LocalGather* g;
+    int rank;
+};
+
+int local_allgather(const void* send, void* recv, size_t bytes, void* user) {
+    auto* R = static_cast<LocalRank*>(user);
+    LocalGather& G = *R->g;
+    std::unique_lock<std::mutex> lk(G.mu);
+    G.slot[size_t(R->rank)].assign(static_cast<const char*>(send), static_cast<const char*>(send) + bytes);
+    G.barrier(lk);
+    for (int r = 0; r < G.world; ++r)
+        std::memcpy(static_cast<char*>(recv) + size_t(r) * bytes, G.slot[size_t(r)].data(), bytes);
+    G.barrier(lk);  // every rank has read before the next iteration overwrites
+    return 0;
+}
+
+struct LocalGroup {
+    LocalGather g;
+    std::vector<LocalRank> ranks;
+    explicit LocalGroup(int w) : g(w), ranks(size_t(w)) {}
+};
+
+}  // namespace
+
+extern "C" {
+
 tcse_ctx* tcse_create_devices(const int32_t* devices, int32_t n_devices) {
     if (!devices || n_devices < 1) {
         fail(TCSE_EINVAL, "tcse_create_devices: need at least one device");
@@ -766,12 +821,36 @@ tcse_ctx* tcse_create_devices(const int32_t* devices, int32_t n_devices) {
     }
     if (n_devices == 1)
         return tcse_create(devices[0]);
+    bool shared = false;
     for (int a = 0; a < n_devices; ++a)
         for (int b = a + 1; b < n_devices; ++b)
-            if (devices[a] == devices[b]) {
-                fail(TCSE_EINVAL, "tcse_create_devices: device %d listed twice", devices[a]);
+            shared = shared || devices[a] == devices[b];
+    if (shared) {
+        if (env_int("TCSE_SHARED_DEVICES", 0) != 1) {
+            fail(TCSE_EINVAL, "tcse_create_devices: a device is listed twice (one rank per GPU)");
+            return nullptr;
+        }
+        // test transport: rank threads exchange through host memory
+        auto* top = tcse_create(devices[0]);
+        if (!top)
+            return nullptr;
+        auto grp = std::make_shared<LocalGroup>(n_devices);
+        top->local_gather = grp;
+        for (int k = 0; k < n_devices; ++k) {
+            tcse_ctx* c = tcse_create(devices[k]);
+            if (!c) {
+                tcse_destroy(top);
                 return nullptr;
             }
+            grp->ranks[size_t(k)] = LocalRank{&grp->g, k};
+            c->rank = k;
+            c->world = n_devices;
+            c->allgather = local_allgather;
+            c->ag_user = &grp->ranks[size_t(k)];
+            top->sub.push_back(c);
+        }
+        return top;
+    }
     const NcclApi& nc = nccl();
     if (!nc.ok) {
         fail(TCSE_ENCCL, "nccl: %s", nc.why);
