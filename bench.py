@@ -25,6 +25,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -96,8 +97,10 @@ def config_block(args, world, scaling="weak"):
         "processes_per_gpu": args.processes,
         "processes_total": args.processes * world,
         "master_seed": args.seed,
-        "parallelism": "process-partition x%d (per-iteration all-gather exchange%s)"
-                       % (world, "" if world == 1 else ", " + str(getattr(args, "dist_backend", "nccl"))),
+        "parallelism": "process-partition x%d (per-iteration payload all-gather%s)"
+                       % (world, "" if world == 1 else (" by the library's ncclAllGather in the iteration graph"
+                                                         if getattr(args, "dist_backend", "nccl") == "nccl"
+                                                         else " through host memory (gloo; ranks share a GPU)")),
         "l2": "flushed before every timed step (256 MiB write)",
     }
 
@@ -170,11 +173,13 @@ def run_reference(args, rank, world):
         C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]
     threads = os.cpu_count() or 1
     _, systems = load_systems(args.workload)
-    # the GPU arm runs processes x gpus per component; the CPU's steps/s does
-    # not depend on the process count once it exceeds the thread count, so the
-    # reference is sampled at up to 16384 processes to bound its run time
-    scheme, _ = load_systems(args.workload)
-    n_proc = min(args.processes * args.gpus, 16384 if scheme["r"] < 100 else 512)
+    # the same process count and iterations as the GPU arm (so the printed
+    # substitution_steps of the two arms can be compared); only multi-GPU
+    # runs are capped (the CPU's steps/s does not depend on the process count
+    # once it exceeds the thread count) to bound the reference's run time
+    n_proc = args.processes * args.gpus
+    if args.gpus > 1:
+        n_proc = min(n_proc, args.processes)
     its = args.warmup + args.steps
     cfg = T.SearchConfig(n_processes=n_proc, patience=1 << 30, master_seed=args.seed, max_iterations=its,
                          forced_strategy=args.strategy).to_c()
@@ -260,42 +265,33 @@ def main():
     local = local % n_dev  # identity with one rank per GPU
     torch.cuda.set_device(local)
     if world > 1:
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group("gloo")
+        # torch.distributed is plumbing only (unique-id broadcast, barriers,
+        # the max-over-ranks timing); the search's own exchange is the
+        # library's ncclAllGather inside the iteration graph
+        dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     dev = T.Device(local)
-    # world > 1: the per-iteration exchange is an NCCL all-gather (NVLink) of
-    # device payloads between tcse_search_step_begin and _end
-    dev.set_partition(rank, world, None)
+    if world > 1 and args.dist_backend == "nccl":
+        uid = [T.Device.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dev.set_nccl(uid[0], rank, world)
+    elif world > 1:
+        # ranks sharing a GPU (NCCL refuses that): host all-gather over gloo
+        def allgather(data):
+            parts = [None] * world
+            dist.all_gather_object(parts, data)
+            return parts
+        dev.set_partition(rank, world, allgather)
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
-    bufs = {}
 
     def step(search):
         """One optimize_system iteration; returns the number of active systems."""
-        if world == 1:
-            return search.step()
-        key = id(search)
-        if key not in bufs:
-            nb = search.payload_bytes()
-            bufs[key] = (torch.empty(nb, dtype=torch.uint8, device="cuda"),
-                         torch.empty(nb * world, dtype=torch.uint8, device="cuda"))
-        send, recv = bufs[key]
-        search.step_begin(send.data_ptr())
-        if args.dist_backend == "nccl":
-            dist.all_gather_into_tensor(recv, send)  # NCCL over NVLink, ordered after the launch stream
-        else:
-            torch.cuda.synchronize()
-            parts = [torch.empty(send.numel(), dtype=torch.uint8) for _ in range(world)]
-            dist.all_gather(parts, send.cpu())
-            recv.copy_(torch.cat(parts))
-        return search.step_end(recv.data_ptr())
+        return search.step()
     _, sys_rows = load_systems(args.workload)
     systems = [T.LinearSystem(nx, rows) for nx, rows in sys_rows]
     n_total = args.processes * world
@@ -324,31 +320,47 @@ def main():
         barrier()
         total_ms += e0.elapsed_time(e1)
     s1 = search.stats()
-    steps_local = s1["steps"] - s0["steps"]
-    kernel_ms = s1["kernel_ms"] - s0["kernel_ms"]
-    wops = s1["wops"] - s0["wops"]
-    launches = s1["launches"] - s0["launches"]
+    delta = lambda k: s1[k] - s0[k]  # noqa: E731
+    steps_local = delta("steps")
+    wops = delta("wops")
+    group = []  # per launch group: search-kernel span (device clock) and word-ops
+    for g in range(s1["n_groups"]):
+        group.append({"nt": s1["group_nt"][g], "words": s1["group_words"][g],
+                      "ms": s1["group_ms"][g] - s0["group_ms"][g], "wops": s1["group_wops"][g] - s0["group_wops"][g]})
+    kernel_ms = delta("kernel_ms")
+    exchange_ms = delta("exchange_ms")
+    launches_counted = delta("kernel_launches")
+    by_strategy = [a - b for a, b in zip(s1["steps_by_strategy"], s0["steps_by_strategy"])]
     results, _ = search.result()
     search.close()
 
-    # ---- e2e: the public call (host CSR in, host records out), K iterations
+    # ---- e2e: the public session API on the product path (the device-
+    # resident loop) over the SAME iterations as `value`: host CSR in (create
+    # uploads the systems), W warm-up iterations untimed, iterations W+1..W+K
+    # as one run() (graph replays, one host synchronisation), host records
+    # out.  Timed: create + run(K) + result, host clock.
     e2e = None
     if not args.no_e2e:
         barrier()
         torch.cuda.synchronize()
+        cfg2 = T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed,
+                              forced_strategy=args.strategy)
         t0 = time.perf_counter()
-        # the public session API: host CSR in (create uploads the systems),
-        # K iterations, host records out
-        s2 = T.Search(systems, T.SearchConfig(n_processes=n_total, patience=1 << 30, master_seed=args.seed,
-                                              max_iterations=args.steps, forced_strategy=args.strategy),
-                      [0, 1, 2], device=dev)
-        while step(s2) > 0:
-            pass
-        _, st = s2.result()
-        s2.close()
+        s2 = T.Search(systems, cfg2, [0, 1, 2], device=dev)
+        t_create = time.perf_counter() - t0
+        s2.run(args.warmup)
+        st_w = s2.stats()
         torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        e2e = {"steps": st["steps"], "secs": e2e_s, "h2d": st["h2d_bytes"], "d2h": st["d2h_bytes"]}
+        t1 = time.perf_counter()
+        s2.run(args.steps)
+        res2, st2 = s2.result()
+        t_run = time.perf_counter() - t1
+        s2.close()
+        e2e = {"steps": st2["steps"] - st_w["steps"], "secs": t_create + t_run,
+               "h2d": st2["h2d_bytes"],  # create's uploads (warm-up iterations copy nothing in)
+               "d2h": st2["d2h_bytes"] - st_w["d2h_bytes"], "syncs": st2["host_syncs"] - st_w["host_syncs"],
+               "graph": st2["graph_launches"] - st_w["graph_launches"],
+               "same_result": [r.cost for r, _ in res2] == [r.cost for r, _ in results]}
     clk = clocks.stop()
     peak_gops = dev.microbench_wordops()
 
@@ -356,12 +368,10 @@ def main():
     vals = torch.tensor([total_ms, float(steps_local), float(wops), kernel_ms,
                          e2e["secs"] if e2e else 0.0, float(e2e["steps"] if e2e else 0)], dtype=torch.float64)
     if world > 1:
-        dev_ = "cuda" if args.dist_backend == "nccl" else "cpu"
-        mx = vals.clone().to(dev_)
-        sm = vals.clone().to(dev_)
+        mx = vals.clone()
+        sm = vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        mx, sm = mx.cpu(), sm.cpu()
     else:
         mx = sm = vals
     if rank != 0:
@@ -371,56 +381,75 @@ def main():
     t_ms = mx[0].item()
     steps_all = sm[1].item()
     value = steps_all / (t_ms / 1e3)
-    # roofline of the dominant kernel (search_kernel): algorithmic word-ops per
-    # launch (SURVEY.md 8(d) model, counted by the kernel) / average launch
-    # duration (CUDA events on the launch stream) vs the measured smem word-op peak
-    per_launch = wops / max(1, launches)
-    avg_launch_ms = kernel_ms / max(1, launches)
-    achieved = per_launch / (avg_launch_ms / 1e3) / 1e9
+    # roofline of the dominant kernel: the search kernel of the launch group
+    # with the longest span (device clock).  achieved = algorithmic word-ops
+    # of that group's processes (SURVEY.md 8(d) model, counted by the kernel)
+    # / its summed launch span, vs the measured smem word-op peak; the other
+    # groups are listed with their own fractions
+    for g in group:
+        g["achieved_gops"] = g["wops"] / (g["ms"] / 1e3) / 1e9 if g["ms"] > 0 else 0.0
+        g["frac"] = g["achieved_gops"] / peak_gops if peak_gops else None
+        g["avg_launch_ms"] = g["ms"] / args.steps
+        g["kernel"] = "search_kernel<W=%d,NT=%d>" % (g["words"], g["nt"])
+    dom = max(group, key=lambda g: g["ms"]) if group else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "search_kernel_dram.json")
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    # the binding resource is instruction issue, not smem bandwidth: the ncu
-    # capture of the same kernel (committed) gives issue / warp occupancy
+    # the binding resource is instruction issue, not smem bandwidth: the
+    # newest committed ncu capture of the same kernel gives issue / occupancy
     issue = None
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True):
-        if name.endswith("_search_kernel_ncu.json"):
-            with open(os.path.join(ROOT, "profiles", name)) as f:
-                nj = json.load(f)
-            pct = lambda k: float(str(nj.get(k, "nan")).split()[0])  # noqa: E731
-            issue = {"issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                     "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
-                     "alu_pipe_pct": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
-                     "lsu_pipe_pct": pct("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
-                     "smem_wavefronts_pct": pct(
-                         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
-                     "source": "profiles/" + name}
-            break
+    caps = []
+    for name in os.listdir(os.path.join(ROOT, "profiles")):
+        m = re.match(r"r(\d+)_v(\d+)_search_kernel_ncu\.json$", name)
+        if m:
+            caps.append(((int(m.group(1)), int(m.group(2))), name))
+    if caps:
+        name = max(caps)[1]
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            nj = json.load(f)
+        pct = lambda k: float(str(nj.get(k, "nan")).split()[0])  # noqa: E731
+        issue = {"issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                 "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                 "alu_pipe_pct": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                 "lsu_pipe_pct": pct("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                 "smem_wavefronts_pct": pct(
+                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                 "source": "profiles/" + name}
     line = {
         "metric": METRIC, "value": value, "unit": "substitution steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (fixed public scheme; search randomness from the seed only)",
         "config": config_block(args, world),
-        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_gops, "unit": "Gword-ops/s",
-                     "frac": achieved / peak_gops if peak_gops else None, "traffic": traffic,
+        "roofline": {"bound": "smem", "achieved": dom["achieved_gops"] if dom else None, "peak": peak_gops,
+                     "unit": "Gword-ops/s", "frac": dom["frac"] if dom else None, "traffic": traffic,
                      "peak_source": "in-repo microbenchmark (tcse_microbench_wordops) on this GPU",
-                     "kernel": "search_kernel<W=1,NT=64>", "kernel_share_of_step": kernel_ms / max(1e-9, total_ms),
+                     "kernel": dom["kernel"] if dom else None,
+                     "groups": group,
+                     "kernel_share_of_step": kernel_ms / max(1e-9, total_ms),
+                     "timing": "device clock (%globaltimer): first block start to last block end of each "
+                               "group's search launch, summed over the timed iterations",
                      "ncu_issue": issue},
         "clocks": clk,
-        # per search launch (one per launch group) prep + place + search, per
-        # iteration pack + reduce
-        "gpu_launches": int(3 * launches + 2 * args.steps),
+        # counted by the library while enqueueing the timed iterations: per
+        # launch group prep + place + search, per iteration pack + tally +
+        # barrier + flags
+        "gpu_launches": int(launches_counted),
         "substitution_steps": int(steps_all),
+        "steps_by_strategy": dict(zip(T.STRATEGY_SHORT, by_strategy)),
+        "exchange_us_per_step": exchange_ms * 1e3 / args.steps,
         "incumbent_costs": [r.cost for r, _ in results],
     }
     if e2e:
         line["e2e"] = {"value": sm[5].item() / mx[4].item(), "unit": "substitution steps/s",
                        "h2d_bytes_per_step": e2e["h2d"] / args.steps, "d2h_bytes_per_step": e2e["d2h"] / args.steps,
-                       "call": "tcse_search_create/step/result (C ABI, host CSR in, host records out), "
-                               "%d iterations" % args.steps}
+                       "call": "tcse_search_create (host CSR in) + tcse_search_run over iterations %d..%d (CUDA "
+                               "graph replays, %d host sync) + tcse_search_result (host records out); the %d "
+                               "warm-up iterations run untimed in the same session"
+                               % (args.warmup + 1, args.warmup + args.steps, e2e["syncs"], args.warmup),
+                       "same_incumbents_as_value_run": e2e["same_result"]}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(args)

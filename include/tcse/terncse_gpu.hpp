@@ -23,6 +23,7 @@
 #include <terncse/parallel_search.hpp>
 
 #include <chrono>
+#include <cstdlib>
 #include <functional>
 #include <memory>
 #include <string>
@@ -32,9 +33,17 @@
 
 namespace terncse::gpu {
 
+// One GPU, or several GPUs of this process as one context: the search then
+// partitions its processes across them with one NCCL all-gather per
+// iteration (tcse_create_devices), results identical to one GPU.
 class Context {
 public:
     explicit Context(int device = 0) : h_(tcse_create(device)) {
+        if (!h_)
+            throw error(tcse_last_error());
+    }
+    explicit Context(const std::vector<int>& devices)
+        : h_(tcse_create_devices(reinterpret_cast<const int32_t*>(devices.data()), int32_t(devices.size()))) {
         if (!h_)
             throw error(tcse_last_error());
     }
@@ -42,13 +51,41 @@ public:
     Context& operator=(const Context&) = delete;
     ~Context() { tcse_destroy(h_); }
     tcse_ctx* get() const { return h_; }
+    int devices() const { return tcse_context_devices(h_); }
 
 private:
     tcse_ctx* h_;
 };
 
+// The default context spans every visible GPU (as the reference's default
+// thread count spans every core, parallel_search.hpp:41-43), or the list in
+// TCSE_DEVICES ("0,1,2,3"); one GPU if NCCL is unavailable.
+inline std::vector<int> default_devices() {
+    std::vector<int> devs;
+    if (const char* env = std::getenv("TCSE_DEVICES")) {
+        std::string s(env), cur;
+        for (char c : s + ",") {
+            if (c == ',') {
+                if (!cur.empty())
+                    devs.push_back(std::stoi(cur));
+                cur.clear();
+            } else {
+                cur += c;
+            }
+        }
+    } else {
+        for (int d = 0; d < tcse_device_count(); ++d)
+            devs.push_back(d);
+    }
+    if (devs.empty())
+        devs.push_back(0);
+    if (devs.size() > 1 && !tcse_nccl_available())
+        devs.resize(1);
+    return devs;
+}
+
 inline Context& default_context() {
-    static Context ctx(0);
+    static Context ctx(default_devices());
     return ctx;
 }
 
