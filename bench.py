@@ -306,7 +306,13 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.15)
-    total_ms = 0.0
+    # each timed step: L2 flush, barrier + synchronize, one iteration (the
+    # captured graph: prep, place, search, pack, [all-gather], barrier
+    # kernels), synchronize + barrier.  Its device time is the library's CUDA
+    # events recorded on the launch stream right before and right after the
+    # iteration's launches (stats step_ms); the outer torch events also span
+    # the host's synchronisation turnaround and are reported beside it.
+    outer_ms = 0.0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     for _ in range(args.steps):
@@ -318,8 +324,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        total_ms += e0.elapsed_time(e1)
+        outer_ms += e0.elapsed_time(e1)
     s1 = search.stats()
+    total_ms = s1["step_ms"] - s0["step_ms"]
     delta = lambda k: s1[k] - s0[k]  # noqa: E731
     steps_local = delta("steps")
     wops = delta("wops")
@@ -429,13 +436,13 @@ def main():
                      "kernel": dom["kernel"] if dom else None,
                      "groups": group,
                      "kernel_share_of_step": kernel_ms / max(1e-9, total_ms),
+                     "host_turnaround_ms_per_step": (outer_ms - total_ms) / args.steps,
                      "timing": "device clock (%globaltimer): first block start to last block end of each "
                                "group's search launch, summed over the timed iterations",
                      "ncu_issue": issue},
         "clocks": clk,
         # counted by the library while enqueueing the timed iterations: per
-        # launch group prep + place + search, per iteration pack + tally +
-        # barrier + flags
+        # launch group prep + place + search, per iteration pack + barrier
         "gpu_launches": int(launches_counted),
         "substitution_steps": int(steps_all),
         "steps_by_strategy": dict(zip(T.STRATEGY_SHORT, by_strategy)),

@@ -195,18 +195,19 @@ struct XchgDesc {
     double fraction;
     int32_t hist_n;
     int32_t patience, max_iterations;
-    // barrier scratch: nblk tally blocks over the n gathered costs
+    // barrier scratch: nblk tally blocks over the n gathered costs; the last
+    // one to arrive (done counter) runs the barrier itself
     int32_t nblk;
-    u64* part_min;     // [nblk] (cost << 32 | p)
+    u64* part_min;       // [nblk] (cost << 32 | p)
     int32_t* part_hist;  // [nblk][hist_n] cost histograms
-    u64* part_sums;    // [nblk][3 + 8]: steps, replayed, word-ops, steps per strategy
-    int32_t* part_off;   // [nblk] ties at the threshold cost before the block
-    int32_t* sel;        // [4]: threshold cost, ties to take, count, improved-rank
+    u64* part_sums;      // [nblk][3 + 8]: steps, replayed, word-ops, steps per strategy
+    int32_t* done;       // arrival counter of this system's tally blocks (reset by the last)
 };
 
 struct XchgLaunch {
     int32_t nsys;
-    int32_t* err;  // the launch error word of this rank (shared with the search launches)
+    int32_t* err;       // the launch error word of this rank (shared with the search launches)
+    int32_t* all_done;  // arrival counter of every barrier block of the launch (clock)
     LoopClock* clock;
     XchgDesc x[kMaxSys];
 };

@@ -253,6 +253,41 @@ __device__ __noinline__ void mt_seed(u64* mt, u64 s) {
     }
 }
 
+// the same seeding straight into the process's shared-memory state (one
+// thread; LDS/STS addressing)
+__device__ __noinline__ void mt_seed_smem(u32 off, u64 s) {
+    u64* mt = reinterpret_cast<u64*>(g_smem + off);
+    u64 x = s;
+    mt[0] = x;
+#pragma unroll 4
+    for (u32 i = 1; i < 312; ++i) {
+        x = kMtF * (x ^ (x >> 62)) + i;
+        mt[i] = x;
+    }
+}
+
+// first output of mt19937_64(s) without storing the state (registers only)
+__device__ __noinline__ u64 mt_first_output(u64 s) {
+    u64 x = s;
+    const u64 x0 = x;
+    x = kMtF * (x ^ (x >> 62)) + 1;
+    const u64 x1 = x;
+#pragma unroll 4
+    for (u32 i = 2; i <= 156; ++i)
+        x = kMtF * (x ^ (x >> 62)) + i;
+    return mt_temper(mt_mix(x0, x1, x));
+}
+
+// the process's stream seed: the slot seed, or mix_seed{slot.seed, comp} in
+// flip mode (parallel_search.hpp:441)
+__device__ __forceinline__ u64 stream_seed(const SysDesc& sd, u64 seed) {
+    if (sd.stream_comp >= 0) {
+        seed = splitmix64(0x5851f42d4c957f2dULL ^ seed);
+        seed = splitmix64(seed ^ u64(sd.stream_comp));
+    }
+    return seed;
+}
+
 // cooperative twist of the 312-word state (block-uniform call), two
 // barriers: thread i owns new[i] = mix(old[i], old[i+1], old[i+156]) and
 // new[156+i] = mix(old[156+i], old[157+i], new[i]); the one cross-thread
@@ -1894,7 +1929,12 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
                 c0[t] = sd.base_cnts[t];
             }
         }
-        if (s_slot.rng) {
+        if (s_slot.rng && !L.rng) {
+            // seed the process's mt19937_64 in shared memory (one thread, while
+            // the others load the base state): no HBM hand-off
+            if (tid == 0)
+                mt_seed_smem(lay.mt, stream_seed(sd, s_slot.seed));
+        } else if (s_slot.rng) {
             // all loads in flight before the stores (2.5 KB from HBM per process)
             constexpr int R = (312 + NT - 1) / NT;
             u64* mt = sp<u64>(lay.mt);
@@ -2075,28 +2115,39 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
 // process will draw — its seeded mt19937_64 state (the 311-step sequential
 // seeding runs here with full-GPU parallelism instead of serially at the
 // start of every search block).
-__global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ LaunchDesc L) {
-    const int b = int(blockIdx.x * blockDim.x + threadIdx.x);
+struct PrepOut {
+    int sys;      // system index in the launch (placement histogram)
+    int st;       // strategy, -1 = nothing to place (no process / skipped)
+    int reinit;   // incumbent length when the process restarts from a prefix
+    bool seed;    // the process draws: seed its stream
+    u64 ps;       // stream seed
+};
+
+__device__ __forceinline__ PrepOut prep_slot(const LaunchDesc& L, int b) {
+    PrepOut o;
+    o.sys = 0;
+    o.st = -1;
+    o.reinit = 0;
+    o.seed = false;
+    o.ps = 0;
     if (b >= L.total_blocks)
-        return;
-    int s = 0;
+        return o;
 #pragma unroll
     for (int t = 1; t < kMaxSys; ++t)
         if (t < L.nsys && b >= L.sys[t].block_begin)
-            s = t;
+            o.sys = t;
     const SysDesc& sd = find_sys(L, b);
     const int lp = b - sd.block_begin;
     if (lp >= sd.n_local)
-        return;
+        return o;
     // the iteration and the incumbent length: from the device loop state in a
     // session (graph replays need no host parameters), else from the descriptor
     int iteration = sd.iteration, inc_len = sd.inc_len;
     if (sd.loop) {
         if (!sd.loop->active || *sd.err != 0) {  // converged system, or the launch already failed
             L.slots[b].strategy = -1;
-            if (L.hist)
-                atomicAdd(&L.hist[s * kHistStride + 7], 1);  // placed last (strategy slot 7 is unused)
-            return;
+            o.st = 7;  // placed last (strategy slot 7 is unused)
+            return o;
         }
         iteration = sd.loop->iteration + 1;
         inc_len = sd.loop->len;
@@ -2137,30 +2188,77 @@ __global__ void __launch_bounds__(128) prep_kernel(const __grid_constant__ Launc
     r.p_greedy = sl.p_greedy;
     r.seed = sl.seed;
     L.slots[b] = r;
-    if (rng) {
-        // optimize_with_flips seeds each (process, component) stream from
-        // mix_seed{slot.seed, comp} (parallel_search.hpp:441)
-        u64 ps = sl.seed;
-        if (sd.stream_comp >= 0) {
-            ps = splitmix64(0x5851f42d4c957f2dULL ^ ps);
-            ps = splitmix64(ps ^ u64(sd.stream_comp));
+    o.st = st;
+    o.reinit = r.reinit;
+    o.seed = rng;
+    o.ps = stream_seed(sd, sl.seed);
+    return o;
+}
+
+// One thread per process: assign_strategies' slot (parallel_search.hpp:
+// 183-205) or the explicit ProcessConfig, the reinit flag, and — when the
+// process will draw and the launch hands states off through HBM — its
+// seeded mt19937_64 state.  The 311-step sequential seeding runs here with
+// full-GPU parallelism instead of on every search block's critical path; the
+// block's 128 states leave through a shared-memory tile, 8 words of every
+// process per round, so each warp store covers whole 64-byte runs instead of
+// 32 scattered words.
+constexpr int kPrepNT = 128;
+constexpr int kSeedChunk = 8;  // 312 = 39 x 8
+
+__global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ LaunchDesc L) {
+    const int b = int(blockIdx.x * blockDim.x + threadIdx.x);
+    const int tid = threadIdx.x;
+    const PrepOut o = prep_slot(L, b);
+    u64 x0 = 0, x1 = 0, x156 = 0;  // for the first output (work class below)
+    if (L.rng) {
+        __shared__ u64 tile[kPrepNT][kSeedChunk + 1];
+        __shared__ unsigned char s_seed[kPrepNT];
+        const int b0 = int(blockIdx.x * blockDim.x);
+        s_seed[tid] = o.seed ? 1 : 0;
+        if (__syncthreads_or(o.seed)) {
+            u64 x = o.ps;
+            x0 = x;
+#pragma unroll 1
+            for (int i0 = 0; i0 < 312; i0 += kSeedChunk) {
+#pragma unroll
+                for (int k = 0; k < kSeedChunk; ++k) {
+                    const int i = i0 + k;
+                    if (i > 0)
+                        x = kMtF * (x ^ (x >> 62)) + u64(i);
+                    if (i == 1)
+                        x1 = x;
+                    if (i == 156)
+                        x156 = x;
+                    tile[tid][k] = x;
+                }
+                __syncthreads();
+                // round r: thread tid writes word (tid % 8) of process r * 16 + tid / 8
+#pragma unroll
+                for (int rr = 0; rr < kSeedChunk; ++rr) {
+                    const int p = rr * (kPrepNT / kSeedChunk) + tid / kSeedChunk, k = tid % kSeedChunk;
+                    const int bp = b0 + p;
+                    if (s_seed[p])
+                        L.rng[size_t(bp) * 312 + size_t(i0 + k)] = tile[p][k];
+                }
+                __syncthreads();
+            }
         }
-        mt_seed(L.rng + size_t(b) * 312, ps);
     }
-    if (L.hist) {
+    if (L.hist && o.st >= 0) {
         // placement bucket (strategy, work class): fresh processes, then reinit
         // ones by the length of their replayed prefix (estimated from the
         // first output of their stream, ignoring the rare rejection: the
         // order never changes results)
         int cls = 0;
-        if (reinit) {
-            const u64* m0 = L.rng + size_t(b) * 312;
-            const u64 x = mt_temper(mt_mix(m0[0], m0[1], m0[156]));
-            const u64 n_pre = 1 + __umul64hi(x, u64(3 * inc_len / 4));
-            cls = 1 + min(3, int(4 * n_pre / u64(inc_len + 1)));
+        if (o.reinit) {
+            const u64 x = L.rng ? mt_temper(mt_mix(x0, x1, x156)) : mt_first_output(o.ps);
+            const u64 n_pre = 1 + __umul64hi(x, u64(3 * o.reinit / 4));
+            cls = 1 + min(3, int(4 * n_pre / u64(o.reinit + 1)));
         }
-        L.slots[b].pad = cls;
-        atomicAdd(&L.hist[s * kHistStride + st + 8 * cls], 1);
+        if (o.st < 7)
+            L.slots[b].pad = cls;
+        atomicAdd(&L.hist[o.sys * kHistStride + o.st + 8 * cls], 1);
     }
 }
 
@@ -2197,26 +2295,25 @@ __global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ Laun
 
 // ----------------------------------------------------------------- K2
 //
-// The iteration barrier (parallel_search.hpp:237-270) as four short kernels
+// The iteration barrier (parallel_search.hpp:237-270) as two short kernels
 // on the launch stream, all reading only device state so a whole iteration
 // can be replayed from a CUDA graph:
-//   pack   — this rank's payload: its slice of costs, its best record, its
-//            launch error;
+//   pack    — this rank's payload: its slice of costs, its best record, its
+//             launch error;
 //   (the payloads are all-gathered here when world > 1: NCCL on the stream)
-//   tally  — nblk blocks per system over the n gathered costs: partial argmin,
-//            per-block cost histograms, this rank's step / word-op sums;
-//   barrier— one block per system: global argmin by (cost, id), strict
-//            improvement, incumbent record copy, patience and max_iterations
-//            (the loop variables of optimize_system), the reinit threshold
-//            cost and the per-block tie offsets for pick_reinit (149-163);
-//   flags  — nblk blocks per system: the next iteration's reinit flags.
+//   barrier — nblk blocks per system tally the n gathered costs (partial
+//             argmin, cost histograms, this rank's step / word-op sums); the
+//             last block to arrive merges them: global argmin by (cost, id),
+//             strict improvement, incumbent record copy, patience and
+//             max_iterations (the loop variables of optimize_system), and the
+//             next reinit flags (pick_reinit, 149-163).
 // A launch error on any rank (device capacity, replay) skips the barrier on
 // every rank, so the host re-runs or reports the same iteration everywhere.
 
 __device__ __forceinline__ int part_of(int n, int world, int r) { return int((long long)n * r / world); }
 
 constexpr int kRedNT = 1024;  // pack / barrier block
-constexpr int kTallyNT = 256;  // tally / flags block
+constexpr int kTallyNT = 256;  // barrier block
 constexpr int kTallyPer = 2048;  // gathered costs per tally block
 
 // owner rank of global process p (contiguous partition)
@@ -2298,269 +2395,285 @@ __global__ void __launch_bounds__(kRedNT) pack_kernel(const __grid_constant__ Xc
     }
 }
 
-// K2b: per-block partials over the gathered costs (grid: nblk x nsys)
-__global__ void __launch_bounds__(kTallyNT) tally_kernel(const __grid_constant__ XchgLaunch XL) {
+// the iteration's device clock (once per iteration, by the last barrier block)
+__device__ void clock_tick(LoopClock* k) {
+    u64 lo = ~0ULL, hi = 0;
+    for (int g = 0; g < kMaxSys; ++g) {
+        if (k->gstart[g] != ~0ULL && k->gend[g] > k->gstart[g]) {
+            k->group_ns[g] += k->gend[g] - k->gstart[g];
+            lo = min(lo, k->gstart[g]);
+            hi = max(hi, k->gend[g]);
+        }
+        k->gstart[g] = ~0ULL;
+        k->gend[g] = 0;
+    }
+    if (hi > lo) {
+        k->search_ns += hi - lo;
+        k->iterations += 1;
+    }
+    const u64 now = globaltimer();
+    if (k->xstart != 0 && now > k->xstart)
+        k->exchange_ns += now - k->xstart;
+    k->xstart = 0;
+}
+
+// K2b: the barrier in one launch (grid: nblk x nsys).  Every block tallies
+// kTallyPer gathered costs (partial argmin, cost histogram) and its share of
+// this rank's step / word-op sums; the last block of a system to arrive runs
+// the barrier: global argmin by (cost, id), strict improvement, incumbent
+// record copy, patience / max_iterations, and the next reinit flags
+// (threshold cost from the merged histogram + ordered tie scan).
+__global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant__ XchgLaunch XL) {
     extern __shared__ int hist[];
     const XchgDesc& X = XL.x[blockIdx.y];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!X.inc->active || *XL.err != 0)
-        return;
-    const int ge = gathered_error(X);
-    if (ge != 0) {  // another rank failed: skip the barrier everywhere
-        if (blockIdx.x == 0 && tid == 0)
-            atomicCAS(XL.err, 0, ge);
-        return;
-    }
-    const int blk = blockIdx.x;
-    for (int v = tid; v < X.hist_n; v += kTallyNT)
-        hist[v] = 0;
-    __syncthreads();
-    const int p0 = blk * kTallyPer, p1 = min(X.n, p0 + kTallyPer);
-    u64 best = ~0ULL;
-    for (int p = p0 + tid; p < p1; p += kTallyNT) {
-        const int c = gathered_cost(X, p);
-        best = min(best, (u64(u32(c)) << 32) | u64(u32(p)));
-        atomicAdd(&hist[min(max(c, 0), X.hist_n - 1)], 1);
-    }
-    // this rank's own processes, same block split over the local slice
+    constexpr int NW = kTallyNT / 32;
     constexpr int kS = 3 + 8;
-    u64 sums[kS];
-#pragma unroll
-    for (int k = 0; k < kS; ++k)
-        sums[k] = 0;
-    const int lper = (X.n_local + gridDim.x - 1) / gridDim.x;
-    const int l0 = min(X.n_local, blk * lper), l1 = min(X.n_local, l0 + lper);
-    for (int t = l0 + tid; t < l1; t += kTallyNT) {
-        const u64 own = u64(X.own[t]);
-        sums[0] += own;
-        sums[1] += u64(X.len[t] - X.own[t]);
-        sums[2] += X.wops[t];
-        const int st = X.strat[t];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            sums[3 + k] += st == k ? own : 0;
+    __shared__ u64 s_red[NW][kS + 1];
+    __shared__ int s_flag[4];
+    const int nb = X.nblk, n = X.n, world = X.world;
+    bool work = X.inc->active && *XL.err == 0;
+    if (work) {
+        const int ge = gathered_error(X);
+        if (ge != 0) {  // another rank failed: skip the barrier everywhere
+            if (blockIdx.x == 0 && tid == 0)
+                atomicCAS(XL.err, 0, ge);
+            work = false;
+        }
     }
-    __shared__ u64 s_red[kTallyNT / 32][kS + 1];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        best = min(best, __shfl_down_sync(FULLMASK, best, o));
-#pragma unroll
-        for (int k = 0; k < kS; ++k)
-            sums[k] += __shfl_down_sync(FULLMASK, sums[k], o);
-    }
-    if (lane == 0) {
-        s_red[warp][0] = best;
-#pragma unroll
-        for (int k = 0; k < kS; ++k)
-            s_red[warp][1 + k] = sums[k];
-    }
-    __syncthreads();
-    if (tid < kS + 1) {
-        u64 v = tid == 0 ? ~0ULL : 0;
-        for (int w = 0; w < kTallyNT / 32; ++w)
-            v = tid == 0 ? min(v, s_red[w][0]) : v + s_red[w][tid];
-        if (tid == 0)
-            X.part_min[blk] = v;
-        else
-            X.part_sums[size_t(blk) * kS + size_t(tid - 1)] = v;
-    }
-    for (int v = tid; v < X.hist_n; v += kTallyNT)
-        X.part_hist[size_t(blk) * size_t(X.hist_n) + size_t(v)] = hist[v];
-}
-
-// K2c: the barrier itself, one block per system
-__global__ void __launch_bounds__(kRedNT) barrier_kernel(const __grid_constant__ XchgLaunch XL) {
-    extern __shared__ int hist[];
-    const XchgDesc& X = XL.x[blockIdx.x];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!X.inc->active || *XL.err != 0)
-        return;
-    __shared__ int s_thr[4];
-    const int n = X.n, world = X.world, nb = X.nblk;
-    if (tid == 0) {
-        u64 b = ~0ULL;
-        constexpr int kS = 3 + 8;
+    bool last = false;
+    if (work) {
+        // ---- tally
+        const int blk = blockIdx.x;
+        for (int v = tid; v < X.hist_n; v += kTallyNT)
+            hist[v] = 0;
+        __syncthreads();
+        const int p0 = blk * kTallyPer, p1 = min(n, p0 + kTallyPer);
+        u64 best = ~0ULL;
+        for (int p = p0 + tid; p < p1; p += kTallyNT) {
+            const int c = gathered_cost(X, p);
+            best = min(best, (u64(u32(c)) << 32) | u64(u32(p)));
+            atomicAdd(&hist[min(max(c, 0), X.hist_n - 1)], 1);
+        }
         u64 sums[kS];
+#pragma unroll
         for (int k = 0; k < kS; ++k)
             sums[k] = 0;
-        for (int k = 0; k < nb; ++k) {
+        const int lper = (X.n_local + nb - 1) / nb;
+        const int l0 = min(X.n_local, blk * lper), l1 = min(X.n_local, l0 + lper);
+        for (int t = l0 + tid; t < l1; t += kTallyNT) {
+            const u64 own = u64(X.own[t]);
+            sums[0] += own;
+            sums[1] += u64(X.len[t] - X.own[t]);
+            sums[2] += X.wops[t];
+            const int st = X.strat[t];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                sums[3 + k] += st == k ? own : 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            best = min(best, __shfl_down_sync(FULLMASK, best, o));
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                sums[k] += __shfl_down_sync(FULLMASK, sums[k], o);
+        }
+        if (lane == 0) {
+            s_red[warp][0] = best;
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                s_red[warp][1 + k] = sums[k];
+        }
+        __syncthreads();
+        if (tid < kS + 1) {
+            u64 v = tid == 0 ? ~0ULL : 0;
+            for (int w = 0; w < NW; ++w)
+                v = tid == 0 ? min(v, s_red[w][0]) : v + s_red[w][tid];
+            if (tid == 0)
+                X.part_min[blk] = v;
+            else
+                X.part_sums[size_t(blk) * kS + size_t(tid - 1)] = v;
+        }
+        for (int v = tid; v < X.hist_n; v += kTallyNT)
+            X.part_hist[size_t(blk) * size_t(X.hist_n) + size_t(v)] = hist[v];
+        // ---- arrival: the last block of this system runs the barrier
+        __threadfence();
+        __syncthreads();
+        if (tid == 0)
+            s_flag[0] = atomicAdd(X.done, 1) == nb - 1 ? 1 : 0;
+        __syncthreads();
+        last = s_flag[0] != 0;
+    }
+    if (last) {
+        __threadfence();  // the other blocks' partials are visible
+        if (tid == 0)
+            *X.done = 0;  // for the next iteration
+        // ---- combine the partials
+        u64 b = ~0ULL;
+        u64 sums[kS];
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            sums[k] = 0;
+        for (int k = tid; k < nb; k += kTallyNT) {
             b = min(b, X.part_min[k]);
+#pragma unroll
             for (int j = 0; j < kS; ++j)
                 sums[j] += X.part_sums[size_t(k) * kS + size_t(j)];
         }
-        // argmin over (cost, global process id): lowest index wins ties (255-260)
-        const int bp = int(b & 0xffffffffu);
-        const int bc = int(b >> 32);
-        const int rb = owner_of(n, world, bp);  // the rank that owns bp carries its record
-        const int32_t* h = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max);
-        IncState* inc = X.inc;
-        inc->best_p = bp;
-        inc->best_cost = bc;
-        inc->steps += sums[0];
-        inc->replayed += sums[1];
-        inc->wops += sums[2];
-        for (int k = 0; k < 8; ++k)
-            inc->steps_by_strategy[k] += sums[3 + k];
-        if (!inc->have || bc < inc->cost) {  // strictly better (261-266)
-            inc->have = 1;
-            inc->cost = bc;
-            inc->len = h[2];
-            inc->strategy = h[3];
-            inc->seed = u64(u32(h[4])) | (u64(u32(h[5])) << 32);
-            inc->improved = 1;
-            inc->unchanged = 0;
-        } else {
-            inc->improved = 0;
-            inc->unchanged += 1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            b = min(b, __shfl_down_sync(FULLMASK, b, o));
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                sums[k] += __shfl_down_sync(FULLMASK, sums[k], o);
         }
-        // the loop condition of optimize_system (268-270) + the stop knob
-        inc->iteration += 1;
-        if (inc->unchanged >= X.patience || (X.max_iterations > 0 && inc->iteration >= X.max_iterations))
-            inc->active = 0;
-        s_thr[0] = inc->improved ? rb : -1;
-        s_thr[1] = inc->len;
-    }
-    __syncthreads();
-    const int rb = s_thr[0];
-    const int inc_len = s_thr[1];
-    if (rb >= 0) {
-        const int32_t* rec = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + kHdr;
-        for (int t = tid; t < inc_len; t += kRedNT)
-            X.inc_keys[t] = u32(rec[t]);
-    }
-    // pick_reinit (149-163) for the next iteration, only if the incumbent can
-    // share a prefix (235-237): histogram of all costs -> threshold cost c*
-    const long long want = llround(__dmul_rn(X.fraction, double(n)));
-    const int count = inc_len >= 2 ? int(min(want, (long long)n)) : 0;
-    if (count <= 0) {
-        if (tid == 0)
-            X.sel[2] = 0;
-        return;
-    }
-    for (int v = tid; v < X.hist_n; v += kRedNT) {
-        int acc = 0;
-        for (int k = 0; k < nb; ++k)
-            acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(v)];
-        hist[v] = acc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        // threshold c*: all costs > c* are chosen, plus the first `need`
-        // processes (by index) with cost == c* (stable order, 158-160);
-        // one warp scans the histogram from the top, 32 costs at a time
-        int acc = 0, cstar = 0, need = 0;
-        for (int top = X.hist_n - 1; top >= 0; top -= 32) {
-            const int c = top - lane;
-            const int hc = c >= 0 ? hist[c] : 0;
-            int incl = hc;  // inclusive scan from the top cost down
+        __syncthreads();  // s_red reuse
+        if (lane == 0) {
+            s_red[warp][0] = b;
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                s_red[warp][1 + k] = sums[k];
+        }
+        // merged histogram (every block's counts)
+        for (int v = tid; v < X.hist_n; v += kTallyNT) {
+            int acc = 0;
+            for (int k = 0; k < nb; ++k)
+                acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(v)];
+            hist[v] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            u64 bb = ~0ULL, ss[kS];
+            for (int k = 0; k < kS; ++k)
+                ss[k] = 0;
+            for (int w = 0; w < NW; ++w) {
+                bb = min(bb, s_red[w][0]);
+                for (int k = 0; k < kS; ++k)
+                    ss[k] += s_red[w][1 + k];
+            }
+            // argmin over (cost, global process id): lowest index wins ties (255-260)
+            const int bp = int(bb & 0xffffffffu);
+            const int bc = int(bb >> 32);
+            const int rb = owner_of(n, world, bp);  // the rank that owns bp carries its record
+            const int32_t* h = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max);
+            IncState* inc = X.inc;
+            inc->best_p = bp;
+            inc->best_cost = bc;
+            inc->steps += ss[0];
+            inc->replayed += ss[1];
+            inc->wops += ss[2];
+            for (int k = 0; k < 8; ++k)
+                inc->steps_by_strategy[k] += ss[3 + k];
+            if (!inc->have || bc < inc->cost) {  // strictly better (261-266)
+                inc->have = 1;
+                inc->cost = bc;
+                inc->len = h[2];
+                inc->strategy = h[3];
+                inc->seed = u64(u32(h[4])) | (u64(u32(h[5])) << 32);
+                inc->improved = 1;
+                inc->unchanged = 0;
+            } else {
+                inc->improved = 0;
+                inc->unchanged += 1;
+            }
+            // the loop condition of optimize_system (268-270) + the stop knob
+            inc->iteration += 1;
+            if (inc->unchanged >= X.patience || (X.max_iterations > 0 && inc->iteration >= X.max_iterations))
+                inc->active = 0;
+            s_flag[0] = inc->improved ? rb : -1;
+            s_flag[1] = inc->len;
+        }
+        __syncthreads();
+        const int rb = s_flag[0];
+        const int inc_len = s_flag[1];
+        if (rb >= 0) {
+            const int32_t* rec =
+                X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + kHdr;
+            for (int t = tid; t < inc_len; t += kTallyNT)
+                X.inc_keys[t] = u32(rec[t]);
+        }
+        // ---- pick_reinit (149-163) for the next iteration, only if the
+        // incumbent can share a prefix (235-237)
+        const long long want = llround(__dmul_rn(X.fraction, double(n)));
+        const int count = inc_len >= 2 ? int(min(want, (long long)n)) : 0;
+        if (count <= 0) {
+            for (int p = tid; p < n; p += kTallyNT)
+                X.reinit_next[p] = 0;
+        } else {
+            if (warp == 0) {
+                // threshold c*: all costs > c* are chosen, plus the first
+                // `need` processes (by index) with cost == c* (stable order,
+                // 158-160); one warp scans the histogram from the top
+                int acc = 0, cstar = 0, need = 0;
+                for (int top = X.hist_n - 1; top >= 0; top -= 32) {
+                    const int c = top - lane;
+                    const int hc = c >= 0 ? hist[c] : 0;
+                    int incl = hc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULLMASK, incl, o);
+                        if (lane >= o)
+                            incl += y;
+                    }
+                    const unsigned hit = __ballot_sync(FULLMASK, c >= 0 && acc + incl >= count);
+                    if (hit) {
+                        const int l = __ffs(hit) - 1;
+                        const int il = __shfl_sync(FULLMASK, incl, l), hl = __shfl_sync(FULLMASK, hc, l);
+                        cstar = top - l;
+                        need = count - (acc + il - hl);
+                        break;
+                    }
+                    acc += __shfl_sync(FULLMASK, incl, 31);
+                }
+                if (lane == 0) {
+                    s_flag[2] = cstar;
+                    s_flag[3] = need;
+                }
+            }
+            __syncthreads();
+            const int cstar = s_flag[2], need = s_flag[3];
+            // every thread a contiguous run of [0, n); ordered tie scan
+            const int E = (n + kTallyNT - 1) / kTallyNT;
+            const int e0 = min(n, tid * E), e1 = min(n, e0 + E);
+            int local = 0;
+            for (int e = e0; e < e1; ++e)
+                local += gathered_cost(X, e) == cstar ? 1 : 0;
+            int incl = local;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(FULLMASK, incl, o);
                 if (lane >= o)
                     incl += y;
             }
-            const unsigned hit = __ballot_sync(FULLMASK, c >= 0 && acc + incl >= count);
-            if (hit) {
-                const int l = __ffs(hit) - 1;
-                const int il = __shfl_sync(FULLMASK, incl, l), hl = __shfl_sync(FULLMASK, hc, l);
-                cstar = top - l;
-                need = count - (acc + il - hl);
-                break;
+            __shared__ int s_w[NW];
+            if (lane == 31)
+                s_w[warp] = incl;
+            __syncthreads();
+            int ex = incl - local;
+            for (int w = 0; w < warp; ++w)
+                ex += s_w[w];
+            for (int e = e0; e < e1; ++e) {
+                const int c = gathered_cost(X, e);
+                u8 f = 0;
+                if (c > cstar) {
+                    f = 1;
+                } else if (c == cstar) {
+                    f = ex < need ? 1 : 0;
+                    ++ex;
+                }
+                X.reinit_next[e] = f;
             }
-            acc += __shfl_sync(FULLMASK, incl, 31);
-        }
-        if (lane == 0) {
-            s_thr[2] = cstar;
-            s_thr[3] = need;
         }
     }
-    __syncthreads();
-    const int cstar = s_thr[2], need = s_thr[3];
-    if (tid == 0) {
-        X.sel[0] = cstar;
-        X.sel[1] = need;
-        X.sel[2] = count;
-        int acc = 0;  // ties at c* before each tally block (index order)
-        for (int k = 0; k < nb; ++k) {
-            X.part_off[k] = acc;
-            acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1))];
+    // ---- the launch's last block (all systems) advances the device clock
+    if (XL.clock) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0 && atomicAdd(XL.all_done, 1) == int(gridDim.x * gridDim.y) - 1) {
+            __threadfence();
+            *XL.all_done = 0;
+            clock_tick(XL.clock);
         }
-    }
-}
-
-// K2d: the next iteration's reinit flags (grid: nblk x nsys)
-__global__ void __launch_bounds__(kTallyNT) flags_kernel(const __grid_constant__ XchgLaunch XL) {
-    const XchgDesc& X = XL.x[blockIdx.y];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && XL.clock) {
-        // the iteration's device clock (once per iteration, before any exit)
-        LoopClock* k = XL.clock;
-        u64 lo = ~0ULL, hi = 0;
-        for (int g = 0; g < kMaxSys; ++g) {
-            if (k->gstart[g] != ~0ULL && k->gend[g] > k->gstart[g]) {
-                k->group_ns[g] += k->gend[g] - k->gstart[g];
-                lo = min(lo, k->gstart[g]);
-                hi = max(hi, k->gend[g]);
-            }
-            k->gstart[g] = ~0ULL;
-            k->gend[g] = 0;
-        }
-        if (hi > lo) {
-            k->search_ns += hi - lo;
-            k->iterations += 1;
-        }
-        const u64 now = globaltimer();
-        if (k->xstart != 0 && now > k->xstart)
-            k->exchange_ns += now - k->xstart;
-        k->xstart = 0;
-    }
-    // a system that just converged keeps its last flags (never read again)
-    if (!X.inc->active || *XL.err != 0)
-        return;
-    const int n = X.n;
-    const int p0 = blockIdx.x * kTallyPer, p1 = min(n, p0 + kTallyPer);
-    if (X.sel[2] <= 0) {
-        for (int p = p0 + tid; p < p1; p += kTallyNT)
-            X.reinit_next[p] = 0;
-        return;
-    }
-    const int cstar = X.sel[0], need = X.sel[1];
-    // each thread a contiguous run of the block's range; ordered tie scan
-    constexpr int kPer = kTallyPer / kTallyNT;
-    const int e0 = min(p1, p0 + tid * kPer), e1 = min(p1, e0 + kPer);
-    int cs[kPer];
-    int local = 0;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        cs[k] = e0 + k < e1 ? gathered_cost(X, e0 + k) : -1;
-        local += cs[k] == cstar ? 1 : 0;
-    }
-    __shared__ int s_w[kTallyNT / 32];
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULLMASK, incl, o);
-        if (lane >= o)
-            incl += y;
-    }
-    if (lane == 31)
-        s_w[warp] = incl;
-    __syncthreads();
-    int ex = X.part_off[blockIdx.x] + incl - local;
-    for (int w = 0; w < warp; ++w)
-        ex += s_w[w];
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-        if (e0 + k >= e1)
-            break;
-        u8 f = 0;
-        if (cs[k] > cstar) {
-            f = 1;
-        } else if (cs[k] == cstar) {
-            f = ex < need ? 1 : 0;
-            ++ex;
-        }
-        X.reinit_next[e0 + k] = f;
     }
 }
 
@@ -2608,7 +2721,7 @@ cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int sm
         if (e != cudaSuccess)
             return e;
     }
-    prep_kernel<<<g, 128, 0, st>>>(L);
+    prep_kernel<<<g, kPrepNT, 0, st>>>(L);
     if (L.perm)
         place_kernel<<<g, 128, 0, st>>>(L);
     cudaError_t e = cudaGetLastError();
@@ -2624,18 +2737,14 @@ cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st) {
 
 int barrier_blocks(int n) { return (n + kTallyPer - 1) / kTallyPer; }
 
-// tally -> barrier -> flags (the exchange, if any, ran before on the stream)
+// the barrier (the exchange, if any, ran before on the stream)
 cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st) {
     const int smem = hist_n * int(sizeof(int));
     const int nb = XL.x[0].nblk;
-    cudaError_t e = cudaFuncSetAttribute(tally_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(barrier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(barrier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
-    tally_kernel<<<dim3(nb, XL.nsys), kTallyNT, smem, st>>>(XL);
-    barrier_kernel<<<XL.nsys, kRedNT, smem, st>>>(XL);
-    flags_kernel<<<dim3(nb, XL.nsys), kTallyNT, 0, st>>>(XL);
+    barrier_kernel<<<dim3(nb, XL.nsys), kTallyNT, smem, st>>>(XL);
     return cudaGetLastError();
 }
 

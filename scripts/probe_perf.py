@@ -18,6 +18,7 @@ st = {}
 t0 = time.time()
 res = T.optimize_systems(systems, cfg, [0, 1, 2], stats=st)
 wall = time.time() - t0
-print("%s N=%d iters=%d forced=%s nt=%s: steps=%d kernel_ms=%.1f wall_ms=%.1f exch_ms=%.1f -> %.3g steps/s (kernel) %.3g steps/s (wall) costs=%s" % (
-    name, N, iters, forced, os.environ.get("TCSE_NT", "64"), st["steps"], st["kernel_ms"], st["wall_ms"], st["exchange_ms"],
-    st["steps"] / st["kernel_ms"] * 1e3, st["steps"] / wall, [r.cost for r, _ in res]))
+print("%s N=%d iters=%d forced=%s nt=%s: steps=%d kernel_ms=%.1f step_ms=%.1f wall_ms=%.1f exch_ms=%.1f -> %.4g steps/s (kernel) %.4g steps/s (step) %.3g steps/s (wall) costs=%s" % (
+    name, N, iters, forced, os.environ.get("TCSE_NT", "64"), st["steps"], st["kernel_ms"], st["step_ms"], st["wall_ms"],
+    st["exchange_ms"], st["steps"] / st["kernel_ms"] * 1e3, st["steps"] / st["step_ms"] * 1e3, st["steps"] / wall,
+    [r.cost for r, _ in res]))
