@@ -398,7 +398,7 @@ int prepare(tcse_ctx* ctx, const tcse_system* s, DevSys* d, int extra_vars = 0) 
 int reserve_prep(tcse_ctx* ctx, int blocks) {
     const size_t b = size_t(std::max(blocks, 1));
     CU(ctx->slots.reserve(b * sizeof(SlotRec)));
-    CU(ctx->rng.reserve(b * 312 * 8));
+    CU(ctx->rng.reserve(b * kCkpt * 8));
     CU(ctx->perm.reserve(b * 4));
     CU(ctx->hist.reserve(sizeof(int32_t) * kHistStride * kMaxSys * (kMaxSys + 1)));
     return TCSE_OK;
@@ -411,7 +411,7 @@ int attach_prep(tcse_ctx* ctx, LaunchDesc* L, int block_offset = 0, int group = 
             return rc;
     }
     L->slots = ctx->slots.as<SlotRec>() + block_offset;
-    L->rng = ctx->rng.as<u64>() + size_t(block_offset) * 312;
+    L->rng = ctx->rng.as<u64>() + size_t(block_offset) * kCkpt;
     // strategy-grouped launch order (search mode; TCSE_ORDER=0 disables)
     static const int order = env_int("TCSE_ORDER", 1);
     if (order && L->sys[0].mode == kModeSearch) {

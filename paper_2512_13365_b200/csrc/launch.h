@@ -18,6 +18,11 @@ typedef uint16_t u16;
 typedef uint8_t u8;
 
 constexpr int kMaxSys = 4;
+// RNG hand-off: the prep kernel runs each process's 311-step mt19937_64
+// seeding chain and keeps every kCkptStride-th state word; the search block
+// restarts kCkpt short chains from them in parallel (one lane each)
+constexpr int kCkpt = 32;
+constexpr int kCkptStride = 10;  // 32 x 10 >= 312
 constexpr int kCoinWords = 512;  // 16384 coin bits per gi scoring chunk
 // placement histogram per system: (strategy, work class) counts, then cursors;
 // class 0 = fresh processes, 1..4 = reinit ones by replayed-prefix quartile
@@ -154,7 +159,7 @@ struct LaunchDesc {
     int32_t nsys;
     int32_t total_blocks;
     SlotRec* slots;  // [total_blocks]
-    u64* rng;        // [total_blocks][312] seeded mt19937_64 states
+    u64* rng;        // [total_blocks][kCkpt] checkpoints of the mt19937_64 seeding chain
     int32_t* perm;   // [total_blocks] launch order -> block (grouped by strategy), or null
     int32_t* hist;   // [kMaxSys][kHistStride] (strategy, work class) histogram + placement cursors
     const SysDesc* table;  // > kMaxSys systems (flip mode): device table, blocks contiguous per system

@@ -1934,19 +1934,20 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             // the others load the base state): no HBM hand-off
             if (tid == 0)
                 mt_seed_smem(lay.mt, stream_seed(sd, s_slot.seed));
-        } else if (s_slot.rng) {
-            // all loads in flight before the stores (2.5 KB from HBM per process)
-            constexpr int R = (312 + NT - 1) / NT;
+        } else if (s_slot.rng && tid < kCkpt) {
+            // 32 checkpoints of the seeding chain (256 B from HBM per process):
+            // lane c restarts the chain at word 10c and fills words 10c..10c+9
             u64* mt = sp<u64>(lay.mt);
-            const u64* src = L.rng + size_t(blk) * 312;
-            u64 v[R];
+            u64 x = __ldg(L.rng + size_t(blk) * kCkpt + size_t(tid));
+            const int i0 = tid * kCkptStride;
+            mt[i0] = x;
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-                v[r] = tid + r * NT < 312 ? __ldg(src + tid + r * NT) : 0ULL;
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                if (tid + r * NT < 312)
-                    mt[tid + r * NT] = v[r];
+            for (int j = 1; j < kCkptStride; ++j) {
+                if (i0 + j >= 312)
+                    break;
+                x = kMtF * (x ^ (x >> 62)) + u64(i0 + j);
+                mt[i0 + j] = x;
+            }
         }
     }
     __syncthreads();
@@ -2197,12 +2198,14 @@ __device__ __forceinline__ PrepOut prep_slot(const LaunchDesc& L, int b) {
 
 // One thread per process: assign_strategies' slot (parallel_search.hpp:
 // 183-205) or the explicit ProcessConfig, the reinit flag, and — when the
-// process will draw and the launch hands states off through HBM — its
-// seeded mt19937_64 state.  The 311-step sequential seeding runs here with
-// full-GPU parallelism instead of on every search block's critical path; the
-// block's 128 states leave through a shared-memory tile, 8 words of every
-// process per round, so each warp store covers whole 64-byte runs instead of
-// 32 scattered words.
+// process will draw and the launch hands states off through HBM — 32
+// checkpoints of its mt19937_64 seeding chain (words 0, 10, ..., 310).  The
+// 311-step sequential chain runs here with full-GPU parallelism; the search
+// block rebuilds the 312-word state from the checkpoints with 32 lanes of
+// 9 steps each, so neither side has the whole chain on its critical path and
+// the hand-off is 256 B per process instead of 2.5 KB.  The checkpoints
+// leave through a shared-memory tile, 8 per process per round, so each warp
+// store covers whole 64-byte runs.
 constexpr int kPrepNT = 128;
 constexpr int kSeedChunk = 8;  // 312 = 39 x 8
 
@@ -2219,27 +2222,30 @@ __global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ L
         if (__syncthreads_or(o.seed)) {
             u64 x = o.ps;
             x0 = x;
+            int i = 0;
 #pragma unroll 1
-            for (int i0 = 0; i0 < 312; i0 += kSeedChunk) {
-#pragma unroll
+            for (int r0 = 0; r0 < kCkpt; r0 += kSeedChunk) {
+#pragma unroll 1
                 for (int k = 0; k < kSeedChunk; ++k) {
-                    const int i = i0 + k;
-                    if (i > 0)
+                    const int target = (r0 + k) * kCkptStride;
+#pragma unroll 1
+                    while (i < target) {
+                        ++i;
                         x = kMtF * (x ^ (x >> 62)) + u64(i);
-                    if (i == 1)
-                        x1 = x;
-                    if (i == 156)
-                        x156 = x;
+                        if (i == 1)
+                            x1 = x;
+                        if (i == 156)
+                            x156 = x;
+                    }
                     tile[tid][k] = x;
                 }
                 __syncthreads();
-                // round r: thread tid writes word (tid % 8) of process r * 16 + tid / 8
+                // thread tid writes checkpoint (tid % 8) of process rr * 16 + tid / 8
 #pragma unroll
                 for (int rr = 0; rr < kSeedChunk; ++rr) {
                     const int p = rr * (kPrepNT / kSeedChunk) + tid / kSeedChunk, k = tid % kSeedChunk;
-                    const int bp = b0 + p;
                     if (s_seed[p])
-                        L.rng[size_t(bp) * 312 + size_t(i0 + k)] = tile[p][k];
+                        L.rng[size_t(b0 + p) * kCkpt + size_t(r0 + k)] = tile[p][k];
                 }
                 __syncthreads();
             }
