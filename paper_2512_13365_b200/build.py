@@ -9,7 +9,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libtcse.so")
+# TCSE_BUILD_OUT / TCSE_NVCC_FLAGS: variant builds for A/B timing (scripts/)
+OUT = os.environ.get("TCSE_BUILD_OUT") or os.path.join(HERE, "libtcse.so")
 SOURCES = ["search.cu", "host.cpp", "microbench.cu", "verify.cu", "nccl_dyn.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -36,8 +37,9 @@ def build(force=False, verbose=False):
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
-        cmd = [NVCC] + FLAGS + ["-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = OUT + "." + src + ".o"
+        extra = os.environ.get("TCSE_NVCC_FLAGS", "").split()
+        cmd = [NVCC] + FLAGS + extra + ["-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     logs = []
@@ -53,7 +55,7 @@ def build(force=False, verbose=False):
     os.replace(OUT + ".tmp", OUT)
     for o in objs:
         os.remove(o)
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    with open(OUT.replace(".so", "") + ".build.log" if os.environ.get("TCSE_BUILD_OUT") else os.path.join(HERE, "build.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))

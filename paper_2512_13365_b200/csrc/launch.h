@@ -231,6 +231,12 @@ struct Lay {
 
 __host__ __device__ inline u32 al16(u32 x) { return (x + 15u) & ~15u; }
 
+// row stride (u32 words) of the per-variable candidate bitmaps: odd, so the
+// rows of 32 different variables start in 32 different shared-memory banks
+// (an even stride of 8 words put them in 4 banks: 8-way conflicts on every
+// row access)
+__host__ __device__ inline u32 bm_stride(int mcap) { return (u32(mcap + 31) >> 5) | 1u; }
+
 __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, int n_e, int coin_words,
                                       int gi_dense, int gi_bm) {
     const u32 NW = u32(nt / 32);
@@ -283,7 +289,7 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
         o += al16((mc + 1u) * 4u);
         L->bm = o;
         if (gi_bm)
-            o += al16((vc + 1u) * ((mc + 31u) / 32u) * 4u);
+            o += al16((vc + 1u) * bm_stride(mcap) * 4u);
         L->nB = L->aoff = L->bs = L->cursor = L->alist = L->nA;
     }
     L->wbt = o;

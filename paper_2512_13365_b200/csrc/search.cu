@@ -493,9 +493,12 @@ __device__ __noinline__ u32 mt_coin_run(u32* coin, u32 pos0, u32 nbits) {
     return n_t;
 }
 
+#ifndef TCSE_TWIST_REG_MIN
+#define TCSE_TWIST_REG_MIN TCSE_FUSED_TWIST_MIN  // block sizes twisting in registers (2 barriers)
+#endif
 template <int NT>
 __device__ __forceinline__ void mt_twist() {
-    if constexpr (NT >= TCSE_FUSED_TWIST_MIN)
+    if constexpr (NT >= TCSE_TWIST_REG_MIN)
         mt_twist_impl<NT, false>(nullptr, 0u, 0u);
     else
         mt_twist_small<NT>();
@@ -1006,7 +1009,7 @@ struct St {
         double* wbt = sp<double>(lay.wbt);
         const u32* coin = sp<u32>(lay.coin);
         // @region gi_zero
-        const int nwl = (mcap + 31) >> 5;  // bitmap row stride (words)
+        const int nwl = int(bm_stride(mcap));  // bitmap row stride (words)
         const int nwm = (m + 31) >> 5;     // words in use this step
         u32* bm = sp<u32>(lay.bm);
 #pragma unroll 1
@@ -1450,7 +1453,7 @@ struct St {
         const u16* c = cnts();
         const u32* coin = sp<u32>(lay.coin);
         const u32 kq = ks[q];
-        const int nwl = (mcap + 31) >> 5;
+        const int nwl = int(bm_stride(mcap));
         const u32* bi = sp<u32>(lay.bm) + key_i(kq) * nwl;
         const u32* bj = sp<u32>(lay.bm) + key_j(kq) * nwl;
         const u32 p = sp<u32>(lay.qbase)[q] - c0;
@@ -1893,9 +1896,15 @@ __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) 
 
 // Register cap: resident processes per SM are bounded by registers before
 // shared memory unless the kernel is held to ~64 registers at 128 threads.
+#ifndef TCSE_MINB32
+#define TCSE_MINB32 28
+#endif
+#ifndef TCSE_MINB64
+#define TCSE_MINB64 14
+#endif
 template <int NT>
 struct MinBlocks {
-    static constexpr int value = NT == 32 ? 28 : (NT == 64 ? 14 : (NT == 128 ? 8 : 4));
+    static constexpr int value = NT == 32 ? TCSE_MINB32 : (NT == 64 ? TCSE_MINB64 : (NT == 128 ? 8 : 4));
 };
 
 template <int W, int NT, bool GID>
