@@ -218,11 +218,12 @@ struct XchgLaunch {
 };
 
 // Shared-memory carve of one process (block).  Byte offsets; the update view
-// (candidate merge scratch) and the gi view (adjacency lists, prefix sums,
-// coin bits) are never live at the same time and share one region.
+// (candidate merge scratch, including the copy of the old keys the list is
+// rewritten from) and the gi view (adjacency lists, prefix sums, coin bits)
+// are never live at the same time and share one region.
 struct Lay {
-    u32 mask, keys0, keys1, cnts0, cnts1;
-    u32 tcnt, ncp, ncn, aux, newexcl;                               // update view
+    u32 mask, keys0, cnts0;
+    u32 tcnt, ncp, ncn, aux, newexcl, kcopy;                        // update view
     u32 qbase, wp, nA, nB, aoff, bs, cursor, alist, wbt, coin, bm;  // gi view
     u32 mt, red, reds, redi, bcast;
     u32 coin_cap;  // coin bits of the gi view
@@ -244,13 +245,11 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
     u32 o = 0;
     L->mask = o;
     o += al16(vc * 2u * u32(W) * 8u);
+    // one candidate list: the update copies the old keys into its scratch
+    // (kcopy) and rewrites the list in place
     L->keys0 = o;
     o += al16(mc * 4u);
-    L->keys1 = o;
-    o += al16(mc * 4u);
     L->cnts0 = o;
-    o += al16(mc * 2u);
-    L->cnts1 = o;
     o += al16(mc * 2u);
     const u32 uni = o;
     L->tcnt = o;
@@ -263,6 +262,8 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
     o += al16(mc * 4u);
     L->newexcl = o;
     o += al16((vc + 2u) * 4u);
+    L->kcopy = o;
+    o += al16(mc * 4u);
     const u32 end_upd = o;
     o = uni;
     L->qbase = o;

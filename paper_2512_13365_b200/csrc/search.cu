@@ -645,14 +645,13 @@ struct St {
     int tid, lane;
     int V;      // variables alive (n_x + n_f)
     int m;      // candidates
-    int cur;    // candidate buffer
     int cost;   // total_cost (linear_system.hpp:202-204)
     int mti;    // mt19937_64 position (312 = twist pending)
     int rsel;   // reduction buffer selector
     u32 last_coins;
 
-    __device__ __forceinline__ u32* keys() { return sp<u32>(cur ? lay.keys1 : lay.keys0); }
-    __device__ __forceinline__ u16* cnts() { return sp<u16>(cur ? lay.cnts1 : lay.cnts0); }
+    __device__ __forceinline__ u32* keys() { return sp<u32>(lay.keys0); }
+    __device__ __forceinline__ u16* cnts() { return sp<u16>(lay.cnts0); }
     __device__ __forceinline__ u64* P(int v) { return sp<u64>(lay.mask) + size_t(v) * 2 * W; }
     __device__ __forceinline__ u64* N(int v) { return sp<u64>(lay.mask) + size_t(v) * 2 * W + W; }
     __device__ __forceinline__ u32* red() {
@@ -786,6 +785,7 @@ struct St {
         const int k = V;
         const u32* ok = keys();
         const u16* oc = cnts();
+        u32* kc = sp<u32>(lay.kcopy);  // the old keys: the list is rewritten in place below
         u16* tcnt = sp<u16>(lay.tcnt);
         u16* ncp = sp<u16>(lay.ncp);
         u16* ncn = sp<u16>(lay.ncn);
@@ -802,6 +802,7 @@ struct St {
             const int a = key_i(kk), b = key_j(kk);
             const u16 ct = (a == i || a == j || b == i || b == j) ? u16(count_pair<W>(a, b, key_neg(kk))) : oc[t];
             tcnt[t] = ct;
+            kc[t] = kk;
             keep += ct >= 2 ? 1u : 0u;
         }
         // (b) the new variable's pairs (x, k, +/-)
@@ -828,20 +829,21 @@ struct St {
         }
         // survivors' scan, high half: threads that found a repeating (x, k, .)
         const u64 sc = block_scan_ool<NT>(keep | (anynew ? 0x10000u : 0u), red());
+        // (every read of the old list is done: the scan's barrier separates
+        // them from the in-place rewrite, which reads kc / tcnt only)
+        u32* dk = sp<u32>(lay.keys0);
+        u16* dc = sp<u16>(lay.cnts0);
         if ((sc >> 48) == 0) {
             // common case: no pair with k repeats, the list only loses entries
-            u32* dk = sp<u32>(cur ? lay.keys0 : lay.keys1);
-            u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
             u32 o = u32(sc) & 0xffffu;
 #pragma unroll 1
             for (int t = a0; t < a1; ++t)
                 if (tcnt[t] >= 2) {
-                    dk[o] = ok[t];
+                    dk[o] = kc[t];
                     dc[o] = tcnt[t];
                     ++o;
                 }
             __syncthreads();
-            cur ^= 1;
             m = int((sc >> 32) & 0xffffu);
             return true;
         }
@@ -871,13 +873,11 @@ struct St {
             n += (ncp[x] >= 2 ? 1u : 0u) + (ncn[x] >= 2 ? 1u : 0u);
         }
         __syncthreads();
-        u32* dk = sp<u32>(cur ? lay.keys0 : lay.keys1);
-        u16* dc = sp<u16>(cur ? lay.cnts0 : lay.cnts1);
         o = excl & 0xffffu;
 #pragma unroll 1
         for (int t = a0; t < a1; ++t)
             if (tcnt[t] >= 2) {
-                const u32 kk = ok[t];
+                const u32 kk = kc[t];
                 const u32 dest = o + newexcl[key_i(kk)];
                 dk[dest] = kk;
                 dc[dest] = tcnt[t];
@@ -895,7 +895,7 @@ struct St {
                     int lo = 0, hi = m;
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (ok[mid] < bound)
+                        if (kc[mid] < bound)
                             lo = mid + 1;
                         else
                             hi = mid;
@@ -909,7 +909,6 @@ struct St {
             }
         }
         __syncthreads();
-        cur ^= 1;
         m = int(n_old + n_new);
         return true;
     }
@@ -1973,7 +1972,6 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     pr.tid = tid;
     pr.lane = tid & 31;
     pr.V = sd.n_x;
-    pr.cur = 0;
     pr.cost = sd.naive;
     pr.mti = 312;
     pr.rsel = 0;
