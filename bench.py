@@ -370,6 +370,7 @@ def main():
                "same_result": [r.cost for r, _ in res2] == [r.cost for r, _ in results]}
     clk = clocks.stop()
     peak_gops = dev.microbench_wordops()
+    pipes = dev.microbench_pipes()
 
     # ---- cross-rank aggregation (max time, summed work)
     vals = torch.tensor([total_ms, float(steps_local), float(wops), kernel_ms,
@@ -439,7 +440,11 @@ def main():
                      "host_turnaround_ms_per_step": (outer_ms - total_ms) / args.steps,
                      "timing": "device clock (%globaltimer): first block start to last block end of each "
                                "group's search launch, summed over the timed iterations",
-                     "ncu_issue": issue},
+                     "ncu_issue": issue,
+                     "pipe_peaks_gops": pipes,
+                     "pipe_peaks_source": "tcse_microbench_pipes on this GPU: G thread-ops/s of IADD3, LOP3, "
+                                          "POPC(+XOR), SHFL, LDS.32, LDS.64 (8 independent chains per thread, "
+                                          "every SM at full occupancy)"},
         "clocks": clk,
         # counted by the library while enqueueing the timed iterations: per
         # launch group prep + place + search, per iteration pack + barrier

@@ -354,6 +354,12 @@ int tcse_optimize_with_flips(tcse_ctx* ctx, const tcse_scheme* scheme, const tcs
  * (two 8-byte LDS, AND, POPC, accumulate) over every SM.  *gops = Gword-ops/s. */
 int tcse_microbench_wordops(tcse_ctx* ctx, double* gops);
 
+/* Measured integer issue peaks of this device (the search kernel's
+ * instruction mix): gops[0..5] = G thread-operations/s of
+ * IADD3, LOP3, POPC, SHFL, 4-byte LDS and 8-byte LDS, each from 8
+ * independent chains per thread on every SM at full occupancy. */
+int tcse_microbench_pipes(tcse_ctx* ctx, double* gops);
+
 /* Batched scheme verification on the device: for every
  * scheme, check_structure (scheme.hpp:54-62; ternary coefficients, positive
  * dimensions) then verify_brent (scheme.hpp:68-95: every Brent identity,

@@ -88,6 +88,7 @@ def lib():
         L.tcse_verify_record.argtypes = [P(_abi.System), P(_abi.Pair), C.c_int32, P(C.c_int32)]
         L.tcse_set_stream.argtypes = [C.c_void_p, C.c_void_p]
         L.tcse_microbench_wordops.argtypes = [C.c_void_p, P(C.c_double)]
+        L.tcse_microbench_pipes.argtypes = [C.c_void_p, P(C.c_double)]
         L.tcse_search_create.argtypes = [C.c_void_p, C.c_int32, P(_abi.System), P(_abi.SearchConfig),
                                          P(C.c_uint64), _abi.ITER_CB, C.c_void_p, P(C.c_void_p)]
         L.tcse_search_step.argtypes = [C.c_void_p, P(C.c_int32)]
@@ -280,6 +281,14 @@ class Device:
         g = C.c_double()
         _check(lib().tcse_microbench_wordops(self._h, C.byref(g)))
         return g.value
+
+    PIPES = ("iadd3", "lop3", "popc", "shfl", "lds32", "lds64")
+
+    def microbench_pipes(self):
+        """Measured integer issue peaks (G thread-ops/s) per instruction kind."""
+        g = (C.c_double * 6)()
+        _check(lib().tcse_microbench_pipes(self._h, g))
+        return dict(zip(self.PIPES, list(g)))
 
     @property
     def handle(self):

@@ -2645,36 +2645,30 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
             }
             __syncthreads();
             const int cstar = s_flag[2], need = s_flag[3];
-            // every thread a contiguous run of [0, n); ordered tie scan
-            const int E = (n + kTallyNT - 1) / kTallyNT;
-            const int e0 = min(n, tid * E), e1 = min(n, e0 + E);
-            int local = 0;
-            for (int e = e0; e < e1; ++e)
-                local += gathered_cost(X, e) == cstar ? 1 : 0;
-            int incl = local;
+            // ordered tie scan over [0, n) in tiles of kTallyNT consecutive
+            // processes (coalesced loads; ties ranked by ballots and the
+            // per-warp counts of the tile)
+            __shared__ int s_w[2][NW];
+            int base = 0;  // ties before the current tile
+            for (int t0 = 0, it = 0; t0 < n; t0 += kTallyNT, ++it) {
+                const int e = t0 + tid;
+                const int c = e < n ? gathered_cost(X, e) : -1;
+                const bool tie = c == cstar;
+                const unsigned bal = __ballot_sync(FULLMASK, tie);
+                if (lane == 0)
+                    s_w[it & 1][warp] = __popc(bal);
+                __syncthreads();
+                int ex = base + __popc(bal & ((1u << lane) - 1u));
+                int tot = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(FULLMASK, incl, o);
-                if (lane >= o)
-                    incl += y;
-            }
-            __shared__ int s_w[NW];
-            if (lane == 31)
-                s_w[warp] = incl;
-            __syncthreads();
-            int ex = incl - local;
-            for (int w = 0; w < warp; ++w)
-                ex += s_w[w];
-            for (int e = e0; e < e1; ++e) {
-                const int c = gathered_cost(X, e);
-                u8 f = 0;
-                if (c > cstar) {
-                    f = 1;
-                } else if (c == cstar) {
-                    f = ex < need ? 1 : 0;
-                    ++ex;
+                for (int w = 0; w < NW; ++w) {
+                    const int cw = s_w[it & 1][w];
+                    ex += w < warp ? cw : 0;
+                    tot += cw;
                 }
-                X.reinit_next[e] = f;
+                if (e < n)
+                    X.reinit_next[e] = u8(c > cstar || (tie && ex < need));
+                base += tot;
             }
         }
     }
