@@ -207,6 +207,7 @@ struct XchgDesc {
     int32_t* part_hist;  // [nblk][hist_n] cost histograms
     u64* part_sums;      // [nblk][3 + 8]: steps, replayed, word-ops, steps per strategy
     int32_t* done;       // arrival counter of this system's tally blocks (reset by the last)
+    int32_t* sel;        // [4]: reinit threshold cost, ties to take, count (flags kernel)
 };
 
 struct XchgLaunch {

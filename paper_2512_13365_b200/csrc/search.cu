@@ -2609,10 +2609,7 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
         // incumbent can share a prefix (235-237)
         const long long want = llround(__dmul_rn(X.fraction, double(n)));
         const int count = inc_len >= 2 ? int(min(want, (long long)n)) : 0;
-        if (count <= 0) {
-            for (int p = tid; p < n; p += kTallyNT)
-                X.reinit_next[p] = 0;
-        } else {
+        if (count > 0) {
             if (warp == 0) {
                 // threshold c*: all costs > c* are chosen, plus the first
                 // `need` processes (by index) with cost == c* (stable order,
@@ -2644,33 +2641,21 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
                 }
             }
             __syncthreads();
-            const int cstar = s_flag[2], need = s_flag[3];
-            // ordered tie scan over [0, n) in tiles of kTallyNT consecutive
-            // processes (coalesced loads; ties ranked by ballots and the
-            // per-warp counts of the tile)
-            __shared__ int s_w[2][NW];
-            int base = 0;  // ties before the current tile
-            for (int t0 = 0, it = 0; t0 < n; t0 += kTallyNT, ++it) {
-                const int e = t0 + tid;
-                const int c = e < n ? gathered_cost(X, e) : -1;
-                const bool tie = c == cstar;
-                const unsigned bal = __ballot_sync(FULLMASK, tie);
-                if (lane == 0)
-                    s_w[it & 1][warp] = __popc(bal);
-                __syncthreads();
-                int ex = base + __popc(bal & ((1u << lane) - 1u));
-                int tot = 0;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    const int cw = s_w[it & 1][w];
-                    ex += w < warp ? cw : 0;
-                    tot += cw;
+            // publish the threshold and every tally block's tie offset (ties
+            // at c* before the block, index order) for the flags kernel
+            if (tid == 0) {
+                const int cstar = s_flag[2];
+                int acc = 0;
+                for (int k = 0; k < nb; ++k) {
+                    X.part_min[k] = u64(u32(acc));  // reused: ties before block k
+                    acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1))];
                 }
-                if (e < n)
-                    X.reinit_next[e] = u8(c > cstar || (tie && ex < need));
-                base += tot;
+                X.sel[0] = cstar;
+                X.sel[1] = s_flag[3];
             }
         }
+        if (tid == 0)
+            X.sel[2] = count;
     }
     // ---- the launch's last block (all systems) advances the device clock
     if (XL.clock) {
@@ -2681,6 +2666,59 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
             *XL.all_done = 0;
             clock_tick(XL.clock);
         }
+    }
+}
+
+// K2c: the next iteration's reinit flags (grid: nblk x nsys), every block
+// its kTallyPer processes: all costs above the threshold c*, and the first
+// `need` ties at c* in index order (offsets from the barrier's last block)
+__global__ void __launch_bounds__(kTallyNT) flags_kernel(const __grid_constant__ XchgLaunch XL) {
+    const XchgDesc& X = XL.x[blockIdx.y];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kTallyNT / 32;
+    // a converged system (before or at this barrier) never reads its flags
+    if (!X.inc->active || *XL.err != 0)
+        return;
+    const int n = X.n;
+    const int p0 = blockIdx.x * kTallyPer, p1 = min(n, p0 + kTallyPer);
+    if (X.sel[2] <= 0) {
+        for (int p = p0 + tid; p < p1; p += kTallyNT)
+            X.reinit_next[p] = 0;
+        return;
+    }
+    const int cstar = X.sel[0], need = X.sel[1];
+    constexpr int kPer = kTallyPer / kTallyNT;
+    // coalesced loads: element p0 + r * kTallyNT + tid, r = 0..kPer-1; tie
+    // ranks by ballots per row of kTallyNT processes
+    int cs[kPer];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        const int e = p0 + r * kTallyNT + tid;
+        cs[r] = e < p1 ? gathered_cost(X, e) : -1;
+    }
+    __shared__ int s_w[kPer][NW];
+    unsigned bal[kPer];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        bal[r] = __ballot_sync(FULLMASK, cs[r] == cstar);
+        if (lane == 0)
+            s_w[r][warp] = __popc(bal[r]);
+    }
+    __syncthreads();
+    int base = int(X.part_min[blockIdx.x]);
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        int ex = base + __popc(bal[r] & ((1u << lane) - 1u));
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            ex += w < warp ? s_w[r][w] : 0;
+            tot += s_w[r][w];
+        }
+        const int e = p0 + r * kTallyNT + tid;
+        if (e < p1)
+            X.reinit_next[e] = u8(cs[r] > cstar || (cs[r] == cstar && ex < need));
+        base += tot;
     }
 }
 
@@ -2752,6 +2790,7 @@ cudaError_t launch_reduce(const XchgLaunch& XL, int hist_n, cudaStream_t st) {
     if (e != cudaSuccess)
         return e;
     barrier_kernel<<<dim3(nb, XL.nsys), kTallyNT, smem, st>>>(XL);
+    flags_kernel<<<dim3(nb, XL.nsys), kTallyNT, 0, st>>>(XL);
     return cudaGetLastError();
 }
 
