@@ -56,6 +56,7 @@ def run(name, seed=1):
     st = {}
     res = T.optimize_systems(systems, gcfg, [0, 1, 2], on_iteration=on_it, stats=st)
     t_gpu = time.time() - start
+    stopped_first = stopped["flag"]  # the seed loop below reuses on_it
     costs = []
     for sys_, (rec, it) in zip(systems, res):
         ok, cost = T.verify_record(sys_, rec.substitutions)
@@ -83,7 +84,7 @@ def run(name, seed=1):
                       "processes": rj["config"]["n_processes"], "iterations": rj["iterations"],
                       "wall_s": round(t_ref, 3), "threads": os.cpu_count()},
         "gpu": {"total": sum(costs), "components": costs, "processes": N, "iterations": [it for _, it in res],
-                "wall_s": round(t_gpu, 3), "stopped_at_budget": stopped["flag"], "steps": st["steps"],
+                "wall_s": round(t_gpu, 3), "stopped_at_budget": stopped_first, "steps": st["steps"],
                 "steps_per_s_device": st["steps"] / max(1e-9, st["kernel_ms"]) * 1e3},
         "gpu_le_reference": sum(costs) <= rj["total"],
         "gpu_seeds_combined": {"total": sum(best), "components": best, "seeds": seeds, "wall_s": round(t_all, 3),
