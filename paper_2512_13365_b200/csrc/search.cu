@@ -64,6 +64,12 @@ constexpr u64 kMtF = 6364136223846793005ULL;
 #ifndef TCSE_FUSED_TWIST_MIN
 #define TCSE_FUSED_TWIST_MIN 128  // block sizes whose coin generations run register-resident (mt_coin_run)
 #endif
+#ifndef TCSE_GI_BALANCE
+#define TCSE_GI_BALANCE 0  // 1: work-balanced contiguous candidate ranges in the bitmap gi pass
+#endif
+#ifndef TCSE_SMALL_TWIST_COINS
+#define TCSE_SMALL_TWIST_COINS 0  // 1: smaller blocks extract coins inside the smem twist (-6% on A/B)
+#endif
 constexpr u64 kCoinMask = 0x8080000004000200ULL;
 
 __device__ __forceinline__ u64 mt_temper(u64 z) {
@@ -377,6 +383,62 @@ __device__ __noinline__ void mt_twist_small() {
         const int i = 156 + tid + r * NT;
         if (i < 312)
             mt[i] = v[r];
+    }
+    __syncthreads();
+}
+
+// The same twist that also emits the new generation's first n outputs as
+// coin bits at coin positions pos0 + e (each warp's 32 consecutive elements
+// by one ballot, straight from the registers the twist computed them in: no
+// second pass over the state in shared memory)
+__device__ __forceinline__ void coin_ballot(u32* coin, u32 pos0, int e, u32 n, u64 x, int lane) {
+    const u32 bit = u32(e) < n ? (u32(__popcll(x & kCoinMask)) & 1u) : 0u;
+    const u32 ball = __ballot_sync(FULLMASK, bit);
+    if (lane == 0 && ball) {
+        const u32 pos = pos0 + u32(e - lane);
+        const u32 w0 = pos >> 5, sh = pos & 31;
+        atomicOr(&coin[w0], ball << sh);
+        if (sh)
+            atomicOr(&coin[w0 + 1], ball >> (32 - sh));
+    }
+}
+
+template <int NT>
+__device__ __noinline__ void mt_twist_small_coins(u32* coin, u32 pos0, u32 n) {
+    constexpr int R = (156 + NT - 1) / NT;
+    u64* mt = sp<u64>(lay.mt);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    u64 v[R];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        v[r] = i < 156 ? mt_mix(mt[i], mt[i + 1], mt[i + 156]) : 0ULL;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < 156)
+            mt[i] = v[r];
+        if (r * NT < 156)  // warp-uniform: the warp's 32 elements exist in part
+            coin_ballot(coin, pos0, i, i < 156 ? n : 0u, v[r], lane);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = 156 + tid + r * NT;
+        v[r] = i < 312 ? mt_mix(mt[i], mt[i == 311 ? 0 : i + 1], mt[i - 156]) : 0ULL;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = 156 + tid + r * NT;
+        if (i < 312)
+            mt[i] = v[r];
+        if (r * NT < 156)
+            coin_ballot(coin, pos0, i, i < 312 ? n : 0u, v[r], lane);
     }
     __syncthreads();
 }
@@ -710,8 +772,17 @@ struct St {
                     done = nbits;
                     break;
                 } else {
+#if TCSE_SMALL_TWIST_COINS
+                    // twist and extract this generation's coins in one pass
+                    const u32 n = min(312u, nbits - done);
+                    mt_twist_small_coins<NT>(coin, done, n);
+                    mti = int(n);
+                    done += n;
+                    continue;
+#else
                     mt_twist<NT>();
                     mti = 0;
+#endif
                 }
             }
             const u32 n = min(u32(312 - mti), nbits - done);
@@ -1322,9 +1393,32 @@ struct St {
                     int q1 = -1, q2 = -1;
                     bool ovf = false;
                     if (gi_bm) {
+#if TCSE_GI_BALANCE
+                        // contiguous candidate ranges of equal work (coins + a
+                        // per-candidate share) per thread: lanes finish together
+                        const u32 per = 6u;
+                        const u32 total = qbase[q_hi] - c0 + per * u32(q_hi - q_lo);
+                        auto split = [&](u32 target) {
+                            int lo2 = q_lo, hi2 = q_hi;  // first q with work(q) >= target
+                            while (lo2 < hi2) {
+                                const int mid = (lo2 + hi2) >> 1;
+                                if (qbase[mid] - c0 + per * u32(mid - q_lo) < target)
+                                    lo2 = mid + 1;
+                                else
+                                    hi2 = mid;
+                            }
+                            return lo2;
+                        };
+                        const int qa = split(u32((u64(total) * u32(tid)) / NT));
+                        const int qb = tid == NT - 1 ? q_hi : split(u32((u64(total) * u32(tid + 1)) / NT));
+#pragma unroll 1
+                        for (int q = qa; q < qb; ++q)
+                            gi_score_bm(q, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+#else
 #pragma unroll 1
                         for (int q = q_lo + tid; q < q_hi; q += NT)
                             gi_score_bm(q, c0, T, alpha, beta, eps2, lb, q1, h1, q2, h2, ovf);
+#endif
                     } else {
                         for (int qb = q_lo; qb < q_hi;) {
                             if (q_hi - qb > NT) {

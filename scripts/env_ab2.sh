@@ -7,7 +7,7 @@ for spec in "$@"; do
       for e in $envs; do
         lp=""; [ "$l" != cur ] && lp=ab/$l.so
         ee=""; [ "$e" != "-" ] && ee=$e
-        echo -n "[$l $e] "; env TCSE_LIBRARY=$lp $ee timeout 120 python scripts/probe_perf.py $spec 2>&1 | tail -1 | sed 's/  wall_ms=[0-9.]* / ; s/ forced=None//; s/costs=.*//'
+        echo -n "[$l $e] "; env TCSE_LIBRARY=$lp $ee timeout 120 python scripts/probe_perf.py $spec 2>&1 | tail -1 | sed -e 's/ wall_ms=[0-9.]*//' -e 's/ forced=None//' -e 's/costs=.*//'
       done
     done
   done
