@@ -2621,11 +2621,12 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
 #pragma unroll
         for (int k = 0; k < kS; ++k)
             sums[k] = 0;
+        // other blocks' partials: read through L2 (ld.cg), never a stale L1 line
         for (int k = tid; k < nb; k += kTallyNT) {
-            b = min(b, X.part_min[k]);
+            b = min(b, __ldcg(X.part_min + k));
 #pragma unroll
             for (int j = 0; j < kS; ++j)
-                sums[j] += X.part_sums[size_t(k) * kS + size_t(j)];
+                sums[j] += __ldcg(X.part_sums + size_t(k) * kS + size_t(j));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -2645,7 +2646,7 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
         for (int v = tid; v < X.hist_n; v += kTallyNT) {
             int acc = 0;
             for (int k = 0; k < nb; ++k)
-                acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(v)];
+                acc += __ldcg(X.part_hist + size_t(k) * size_t(X.hist_n) + size_t(v));
             hist[v] = acc;
         }
         __syncthreads();
@@ -2742,7 +2743,7 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
                 int acc = 0;
                 for (int k = 0; k < nb; ++k) {
                     X.part_min[k] = u64(u32(acc));  // reused: ties before block k
-                    acc += X.part_hist[size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1))];
+                    acc += __ldcg(X.part_hist + size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1)));
                 }
                 X.sel[0] = cstar;
                 X.sel[1] = s_flag[3];
