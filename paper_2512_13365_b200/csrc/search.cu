@@ -64,6 +64,9 @@ constexpr u64 kMtF = 6364136223846793005ULL;
 #ifndef TCSE_FUSED_TWIST_MIN
 #define TCSE_FUSED_TWIST_MIN 128  // block sizes whose coin generations run register-resident (mt_coin_run)
 #endif
+#ifndef TCSE_ONLY_GI
+#define TCSE_ONLY_GI 0
+#endif
 #ifndef TCSE_GI_BALANCE
 #define TCSE_GI_BALANCE 0  // 1: work-balanced contiguous candidate ranges in the bitmap gi pass
 #endif
@@ -2149,6 +2152,12 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         const u64 Vt = u64(pr.V), mt_ = u64(pr.m);
         int pick;
         u64 sel = mt_;
+#if TCSE_ONLY_GI  // experiment: a Greedy-Intersections-only kernel (code size / registers)
+        if (true) {
+            pick = pr.template sel_gi<GID>(alpha, beta);
+            sel += pr.last_coins;
+        } else
+#endif
         if (strat == TCSE_GREEDY) {
             pick = pr.sel_greedy();
         } else if (strat == TCSE_GREEDY_ALTERNATIVE) {
@@ -2433,13 +2442,19 @@ __device__ __forceinline__ int owner_of(int n, int world, int p) {
     return r;
 }
 
+// direct mode (X.recv == null: one rank, no exchange): the barrier reads the
+// per-process outputs themselves and pack is not launched
 __device__ __forceinline__ int gathered_cost(const XchgDesc& X, int p) {
+    if (!X.recv)
+        return X.cost[p];
     const int r = owner_of(X.n, X.world, p);
     return X.recv[size_t(r) * size_t(X.words_total) + size_t(X.sys_off) + size_t(p - part_of(X.n, X.world, r))];
 }
 
 // first launch error among the gathered payloads (0 = none)
 __device__ __forceinline__ int gathered_error(const XchgDesc& X) {
+    if (!X.recv)
+        return 0;  // the local error word is checked by the caller
     int e = 0;
     for (int r = 0; r < X.world && e == 0; ++r)
         e = X.recv[size_t(r) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + 6];
@@ -2537,8 +2552,10 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
     constexpr int NW = kTallyNT / 32;
     constexpr int kS = 3 + 8;
     __shared__ u64 s_red[NW][kS + 1];
-    __shared__ int s_flag[4];
+    __shared__ int s_flag[6];
     const int nb = X.nblk, n = X.n, world = X.world;
+    if (!X.recv && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && XL.clock && XL.clock->xstart == 0)
+        XL.clock->xstart = globaltimer();  // direct mode: no pack launch stamped it
     bool work = X.inc->active && *XL.err == 0;
     if (work) {
         const int ge = gathered_error(X);
@@ -2663,7 +2680,6 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
             const int bp = int(bb & 0xffffffffu);
             const int bc = int(bb >> 32);
             const int rb = owner_of(n, world, bp);  // the rank that owns bp carries its record
-            const int32_t* h = X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max);
             IncState* inc = X.inc;
             inc->best_p = bp;
             inc->best_cost = bc;
@@ -2675,9 +2691,17 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
             if (!inc->have || bc < inc->cost) {  // strictly better (261-266)
                 inc->have = 1;
                 inc->cost = bc;
-                inc->len = h[2];
-                inc->strategy = h[3];
-                inc->seed = u64(u32(h[4])) | (u64(u32(h[5])) << 32);
+                if (X.recv) {
+                    const int32_t* h =
+                        X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max);
+                    inc->len = h[2];
+                    inc->strategy = h[3];
+                    inc->seed = u64(u32(h[4])) | (u64(u32(h[5])) << 32);
+                } else {
+                    inc->len = X.len[bp];
+                    inc->strategy = X.strat[bp];
+                    inc->seed = X.seed[bp];
+                }
                 inc->improved = 1;
                 inc->unchanged = 0;
             } else {
@@ -2690,15 +2714,22 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
                 inc->active = 0;
             s_flag[0] = inc->improved ? rb : -1;
             s_flag[1] = inc->len;
+            s_flag[4] = bp;  // (direct mode: the best process's record row)
         }
         __syncthreads();
         const int rb = s_flag[0];
         const int inc_len = s_flag[1];
         if (rb >= 0) {
-            const int32_t* rec =
-                X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + kHdr;
-            for (int t = tid; t < inc_len; t += kTallyNT)
-                X.inc_keys[t] = u32(rec[t]);
+            if (X.recv) {
+                const int32_t* rec =
+                    X.recv + size_t(rb) * size_t(X.words_total) + size_t(X.sys_off) + size_t(X.n_max) + kHdr;
+                for (int t = tid; t < inc_len; t += kTallyNT)
+                    X.inc_keys[t] = u32(rec[t]);
+            } else {
+                const u32* rec = X.subs + size_t(s_flag[4]) * size_t(X.sub_cap);
+                for (int t = tid; t < inc_len; t += kTallyNT)
+                    X.inc_keys[t] = rec[t];
+            }
         }
         // ---- pick_reinit (149-163) for the next iteration, only if the
         // incumbent can share a prefix (235-237)
