@@ -2361,52 +2361,81 @@ __global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ L
             }
         }
     }
-    if (L.hist && o.st >= 0) {
+    if (L.hist) {
         // placement bucket (strategy, work class): fresh processes, then reinit
         // ones by the length of their replayed prefix (estimated from the
         // first output of their stream, ignoring the rare rejection: the
-        // order never changes results)
-        int cls = 0;
-        if (o.reinit) {
-            const u64 x = L.rng ? mt_temper(mt_mix(x0, x1, x156)) : mt_first_output(o.ps);
-            const u64 n_pre = 1 + __umul64hi(x, u64(3 * o.reinit / 4));
-            cls = 1 + min(3, int(4 * n_pre / u64(o.reinit + 1)));
+        // order never changes results).  Counted per block in shared memory
+        // first: one global atomic per non-empty bucket and block instead of
+        // one per process on a handful of addresses
+        constexpr int kBuckets = 8 * kWorkClasses;
+        __shared__ int s_h[kMaxSys * kBuckets];
+        for (int t = tid; t < kMaxSys * kBuckets; t += kPrepNT)
+            s_h[t] = 0;
+        __syncthreads();
+        if (o.st >= 0) {
+            int cls = 0;
+            if (o.reinit) {
+                const u64 x = L.rng ? mt_temper(mt_mix(x0, x1, x156)) : mt_first_output(o.ps);
+                const u64 n_pre = 1 + __umul64hi(x, u64(3 * o.reinit / 4));
+                cls = 1 + min(3, int(4 * n_pre / u64(o.reinit + 1)));
+            }
+            if (o.st < 7)
+                L.slots[b].pad = cls;
+            atomicAdd(&s_h[o.sys * kBuckets + o.st + 8 * cls], 1);
         }
-        if (o.st < 7)
-            L.slots[b].pad = cls;
-        atomicAdd(&L.hist[o.sys * kHistStride + o.st + 8 * cls], 1);
+        __syncthreads();
+        for (int t = tid; t < kMaxSys * kBuckets; t += kPrepNT)
+            if (s_h[t])
+                atomicAdd(&L.hist[(t / kBuckets) * kHistStride + (t % kBuckets)], s_h[t]);
     }
 }
 
 // launch position of every block: per system, strategies in the order
 // gp, gi, mix, gr, ga, wr, g (roughly decreasing cost), any order within one
 __global__ void __launch_bounds__(128) place_kernel(const __grid_constant__ LaunchDesc L) {
-    const int b = int(blockIdx.x * blockDim.x + threadIdx.x);
-    if (b >= L.total_blocks)
-        return;
-    int s = 0;
+    constexpr int kBuckets = 8 * kWorkClasses;
+    __shared__ int s_cnt[kMaxSys * kBuckets];
+    __shared__ int s_base[kMaxSys * kBuckets];
+    const int tid = threadIdx.x;
+    const int b = int(blockIdx.x * blockDim.x + tid);
+    for (int t = tid; t < kMaxSys * kBuckets; t += 128)
+        s_cnt[t] = 0;
+    __syncthreads();
+    int s = 0, bucket = -1, rank = 0, base = 0;
+    if (b < L.total_blocks) {
 #pragma unroll
-    for (int t = 1; t < kMaxSys; ++t)
-        if (t < L.nsys && b >= L.sys[t].block_begin)
-            s = t;
-    const SysDesc& sd = L.sys[s];
-    if (b - sd.block_begin >= sd.n_local)
-        return;
-    const int order[8] = {TCSE_GREEDY_POTENTIAL, TCSE_GREEDY_INTERSECTIONS, TCSE_MIXED, TCSE_GREEDY_RANDOM,
-                          TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY, 7};
-    // within a strategy, fresh processes before reinit ones (which replay part
-    // of the incumbent instead of selecting: shorter); skipped blocks (slot 7) last
-    const int st0 = L.slots[b].strategy;
-    const int st = st0 < 0 ? 7 : st0, cls = st0 < 0 ? 0 : L.slots[b].pad;
-    const int* h = L.hist + s * kHistStride;
-    int base = sd.block_begin;
-    for (int k = 0; k < 8 && order[k] != st; ++k)
+        for (int t = 1; t < kMaxSys; ++t)
+            if (t < L.nsys && b >= L.sys[t].block_begin)
+                s = t;
+        const SysDesc& sd = L.sys[s];
+        if (b - sd.block_begin < sd.n_local) {
+            const int order[8] = {TCSE_GREEDY_POTENTIAL, TCSE_GREEDY_INTERSECTIONS, TCSE_MIXED, TCSE_GREEDY_RANDOM,
+                                  TCSE_GREEDY_ALTERNATIVE, TCSE_WEIGHTED_RANDOM, TCSE_GREEDY, 7};
+            // within a strategy, fresh processes before reinit ones (which
+            // replay part of the incumbent instead of selecting: shorter);
+            // skipped blocks (slot 7) last
+            const int st0 = L.slots[b].strategy;
+            const int st = st0 < 0 ? 7 : st0, cls = st0 < 0 ? 0 : L.slots[b].pad;
+            const int* h = L.hist + s * kHistStride;
+            base = sd.block_begin;
+            for (int k = 0; k < 8 && order[k] != st; ++k)
 #pragma unroll
-        for (int c = 0; c < kWorkClasses; ++c)
-            base += h[order[k] + 8 * c];
-    for (int c = 0; c < cls; ++c)
-        base += h[st + 8 * c];
-    L.perm[base + atomicAdd(&L.hist[s * kHistStride + 8 * kWorkClasses + st + 8 * cls], 1)] = b;
+                for (int c = 0; c < kWorkClasses; ++c)
+                    base += h[order[k] + 8 * c];
+            for (int c = 0; c < cls; ++c)
+                base += h[st + 8 * c];
+            bucket = s * kBuckets + st + 8 * cls;
+            rank = atomicAdd(&s_cnt[bucket], 1);  // any order within a bucket
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < kMaxSys * kBuckets; t += 128)
+        if (s_cnt[t])
+            s_base[t] = atomicAdd(&L.hist[(t / kBuckets) * kHistStride + 8 * kWorkClasses + (t % kBuckets)], s_cnt[t]);
+    __syncthreads();
+    if (bucket >= 0)
+        L.perm[base + s_base[bucket] + rank] = b;
 }
 
 // ----------------------------------------------------------------- K2
@@ -2517,26 +2546,35 @@ __global__ void __launch_bounds__(kRedNT) pack_kernel(const __grid_constant__ Xc
     }
 }
 
-// the iteration's device clock (once per iteration, by the last barrier block)
-__device__ void clock_tick(LoopClock* k) {
+// the iteration's device clock (once per iteration, by the last barrier
+// block's first warp: lane g < kMaxSys handles launch group g)
+__device__ void clock_tick(LoopClock* k, int lane) {
     u64 lo = ~0ULL, hi = 0;
-    for (int g = 0; g < kMaxSys; ++g) {
-        if (k->gstart[g] != ~0ULL && k->gend[g] > k->gstart[g]) {
-            k->group_ns[g] += k->gend[g] - k->gstart[g];
-            lo = min(lo, k->gstart[g]);
-            hi = max(hi, k->gend[g]);
+    if (lane < kMaxSys) {
+        const u64 g0 = __ldcg(k->gstart + lane), g1 = __ldcg(k->gend + lane);
+        if (g0 != ~0ULL && g1 > g0) {
+            k->group_ns[lane] += g1 - g0;
+            lo = g0;
+            hi = g1;
         }
-        k->gstart[g] = ~0ULL;
-        k->gend[g] = 0;
+        k->gstart[lane] = ~0ULL;
+        k->gend[lane] = 0;
     }
-    if (hi > lo) {
-        k->search_ns += hi - lo;
-        k->iterations += 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULLMASK, lo, o));
+        hi = max(hi, __shfl_xor_sync(FULLMASK, hi, o));
     }
-    const u64 now = globaltimer();
-    if (k->xstart != 0 && now > k->xstart)
-        k->exchange_ns += now - k->xstart;
-    k->xstart = 0;
+    if (lane == 0) {
+        if (hi > lo) {
+            k->search_ns += hi - lo;
+            k->iterations += 1;
+        }
+        const u64 now = globaltimer(), x0 = __ldcg(&k->xstart);
+        if (x0 != 0 && now > x0)
+            k->exchange_ns += now - x0;
+        k->xstart = 0;
+    }
 }
 
 // K2b: the barrier in one launch (grid: nblk x nsys).  Every block tallies
@@ -2769,15 +2807,29 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
             __syncthreads();
             // publish the threshold and every tally block's tie offset (ties
             // at c* before the block, index order) for the flags kernel
-            if (tid == 0) {
+            if (warp == 0) {
                 const int cstar = s_flag[2];
-                int acc = 0;
-                for (int k = 0; k < nb; ++k) {
-                    X.part_min[k] = u64(u32(acc));  // reused: ties before block k
-                    acc += __ldcg(X.part_hist + size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1)));
+                int acc = 0;  // ties at c* before block k (part_min reused for it)
+                for (int k0 = 0; k0 < nb; k0 += 32) {
+                    const int k = k0 + lane;
+                    const int v =
+                        k < nb ? __ldcg(X.part_hist + size_t(k) * size_t(X.hist_n) + size_t(min(cstar, X.hist_n - 1)))
+                               : 0;
+                    int incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(FULLMASK, incl, o);
+                        if (lane >= o)
+                            incl += y;
+                    }
+                    if (k < nb)
+                        X.part_min[k] = u64(u32(acc + incl - v));
+                    acc += __shfl_sync(FULLMASK, incl, 31);
                 }
-                X.sel[0] = cstar;
-                X.sel[1] = s_flag[3];
+                if (lane == 0) {
+                    X.sel[0] = cstar;
+                    X.sel[1] = s_flag[3];
+                }
             }
         }
         if (tid == 0)
@@ -2787,10 +2839,14 @@ __global__ void __launch_bounds__(kTallyNT) barrier_kernel(const __grid_constant
     if (XL.clock) {
         __threadfence();
         __syncthreads();
-        if (tid == 0 && atomicAdd(XL.all_done, 1) == int(gridDim.x * gridDim.y) - 1) {
+        if (tid == 0)
+            s_flag[5] = atomicAdd(XL.all_done, 1) == int(gridDim.x * gridDim.y) - 1 ? 1 : 0;
+        __syncthreads();
+        if (s_flag[5] && warp == 0) {
             __threadfence();
-            *XL.all_done = 0;
-            clock_tick(XL.clock);
+            if (lane == 0)
+                *XL.all_done = 0;
+            clock_tick(XL.clock, lane);
         }
     }
 }
