@@ -99,7 +99,7 @@ typedef struct tcse_process_config {
 } tcse_process_config;
 
 /* SearchConfig (parallel_search.hpp:44-53) minus flip mode and threads, plus
- * two stop knobs that are not in the reference (0 = off).  Call
+ * three stop knobs that are not in the reference (0 = off).  Call
  * tcse_default_search_config() to get the reference defaults. */
 typedef struct tcse_search_config {
     int32_t n_processes; /* 0 = 256, as optimize_system does (parallel_search.hpp:224) */
@@ -110,6 +110,11 @@ typedef struct tcse_search_config {
     int32_t forced_strategy; /* -1 = none (draw from weights) */
     int32_t max_iterations;  /* 0 = until patience (reference behaviour) */
     double mix_weights[4];   /* ProcessConfig default {8,4,2,1} */
+    double wall_budget_s;    /* 0 = none; else every system stops at the first iteration
+                                barrier after this much device time from the search's first
+                                launch — the fixed-wall-time run SURVEY.md 8(d) drives through
+                                on_iteration, decided on the device (rank 0's clock for every
+                                rank), so it needs no host turn per iteration */
 } tcse_search_config;
 
 /* SolutionRecord (cse_engine.hpp:18-23).  subs is caller-allocated with room

@@ -169,20 +169,20 @@ class SearchConfig(dict):
 
     def __init__(self, n_processes=0, strategy_weights=DEFAULT_WEIGHTS, reinit_fraction=0.40, patience=10,
                  master_seed=0, forced_strategy=None, max_iterations=0, mix_weights=DEFAULT_MIX,
-                 flip_enabled=False, m_schemes=32, flips_min=1, flips_max=16):
+                 flip_enabled=False, m_schemes=32, flips_min=1, flips_max=16, wall_budget_s=0.0):
         if isinstance(forced_strategy, str):
             forced_strategy = strategy_from_string(forced_strategy)
         super().__init__(n_processes=n_processes, strategy_weights=tuple(strategy_weights),
                          reinit_fraction=reinit_fraction, patience=patience, master_seed=master_seed,
                          forced_strategy=forced_strategy, max_iterations=max_iterations,
                          mix_weights=tuple(mix_weights), flip_enabled=flip_enabled, m_schemes=m_schemes,
-                         flips_min=flips_min, flips_max=flips_max)
+                         flips_min=flips_min, flips_max=flips_max, wall_budget_s=wall_budget_s)
 
     def to_c(self):
         f = self["forced_strategy"]
         return make_search_config(self["n_processes"], self["strategy_weights"], self["reinit_fraction"],
                                   self["patience"], self["master_seed"], -1 if f is None else f,
-                                  self["max_iterations"], self["mix_weights"])
+                                  self["max_iterations"], self["mix_weights"], self.get("wall_budget_s", 0.0))
 
 
 class SolutionRecord:

@@ -64,6 +64,7 @@ class SearchConfig(C.Structure):
         ("forced_strategy", C.c_int32),
         ("max_iterations", C.c_int32),
         ("mix_weights", C.c_double * 4),
+        ("wall_budget_s", C.c_double),
     ]
 
 
@@ -169,7 +170,8 @@ def record_subs(rec):
 
 
 def make_search_config(n_processes=0, weights=DEFAULT_WEIGHTS, reinit_fraction=0.40, patience=10,
-                       master_seed=0, forced_strategy=-1, max_iterations=0, mix_weights=DEFAULT_MIX):
+                       master_seed=0, forced_strategy=-1, max_iterations=0, mix_weights=DEFAULT_MIX,
+                       wall_budget_s=0.0):
     cfg = SearchConfig()
     cfg.n_processes = n_processes
     cfg.patience = patience
@@ -181,6 +183,7 @@ def make_search_config(n_processes=0, weights=DEFAULT_WEIGHTS, reinit_fraction=0
     cfg.max_iterations = max_iterations
     for k in range(4):
         cfg.mix_weights[k] = float(mix_weights[k])
+    cfg.wall_budget_s = float(wall_budget_s)
     return cfg
 
 

@@ -566,6 +566,8 @@ int validate_config(const tcse_search_config* c) {
         return fail(TCSE_EINVAL, "search config: reinit_fraction must be in [0, 1]");
     if (c->patience < 1)
         return fail(TCSE_EINVAL, "search config: patience must be >= 1");
+    if (!(c->wall_budget_s >= 0.0))
+        return fail(TCSE_EINVAL, "search config: wall_budget_s must be >= 0");
     if (c->forced_strategy < -1 || c->forced_strategy >= TCSE_STRATEGY_COUNT)
         return fail(TCSE_EINVAL, "search config: unknown forced strategy %d", c->forced_strategy);
     if (c->forced_strategy < 0) {

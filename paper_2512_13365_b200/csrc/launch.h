@@ -77,6 +77,7 @@ struct LoopClock {
     u64 search_ns;    // union of the iteration's search-group spans
     u64 exchange_ns;  // pack -> end of the barrier kernels
     u64 iterations;   // iterations the clock saw
+    u64 t_begin;      // the search's first launch (wall budget origin)
 };
 
 struct SysDesc {
@@ -177,6 +178,8 @@ struct LaunchDesc {
 //   n_max + 6             the rank's launch error (0 = none): every rank then
 //                         skips the barrier and reports it (a capacity retry
 //                         re-runs the iteration on every rank)
+//   n_max + 7             1 if the rank's clock passed the wall budget at pack
+//                         time (rank 0's word stops every rank)
 //   n_max + kHdr ..       its record (u32 pair keys), sub_cap entries
 // With world = 1 the gathered buffer is this payload itself, so one code
 // path serves every world size.
@@ -215,6 +218,7 @@ struct XchgLaunch {
     int32_t* err;       // the launch error word of this rank (shared with the search launches)
     int32_t* all_done;  // arrival counter of every barrier block of the launch (clock)
     LoopClock* clock;
+    u64 budget_ns;      // wall budget (0 = none): rank 0's clock decides for every rank
     XchgDesc x[kMaxSys];
 };
 

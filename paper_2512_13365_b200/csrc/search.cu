@@ -2322,6 +2322,8 @@ constexpr int kSeedChunk = 8;  // 312 = 39 x 8
 __global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ LaunchDesc L) {
     const int b = int(blockIdx.x * blockDim.x + threadIdx.x);
     const int tid = threadIdx.x;
+    if (b == 0 && L.clock && L.group == 0 && L.clock->t_begin == 0)
+        L.clock->t_begin = globaltimer();  // the search's first launch
     const PrepOut o = prep_slot(L, b);
     u64 x0 = 0, x1 = 0, x156 = 0;  // for the first output (work class below)
     if (L.rng) {
@@ -2533,7 +2535,7 @@ __global__ void __launch_bounds__(kRedNT) pack_kernel(const __grid_constant__ Xc
         h[4] = int32_t(u32(sd));
         h[5] = int32_t(u32(sd >> 32));
         h[6] = 0;
-        h[7] = 0;
+        h[7] = (XL.budget_ns && XL.clock && globaltimer() - XL.clock->t_begin >= XL.budget_ns) ? 1 : 0;
         s_bp = t;
     }
     __syncthreads();
@@ -2858,6 +2860,21 @@ __global__ void __launch_bounds__(kTallyNT) flags_kernel(const __grid_constant__
     const XchgDesc& X = XL.x[blockIdx.y];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = kTallyNT / 32;
+    if (XL.budget_ns && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && *XL.err == 0) {
+        // the fixed-wall-time stop (at the first barrier after the budget):
+        // every system of the session at once; with an exchange, rank 0's
+        // clock as it travelled in its payload, so every rank agrees
+        bool stop = false;
+        if (!X.recv) {
+            stop = globaltimer() - XL.clock->t_begin >= XL.budget_ns;
+        } else {
+            for (int s = 0; s < XL.nsys; ++s)
+                stop = stop || XL.x[s].recv[size_t(XL.x[s].sys_off) + size_t(XL.x[s].n_max) + 7] != 0;
+        }
+        if (stop)
+            for (int s = 0; s < XL.nsys; ++s)
+                XL.x[s].inc->active = 0;
+    }
     // a converged system (before or at this barrier) never reads its flags
     if (!X.inc->active || *XL.err != 0)
         return;

@@ -151,3 +151,42 @@ def test_multi_device_context_shared_gpu(world):
 def test_duplicate_devices_refused():
     with pytest.raises(T.TcseError, match="listed twice"):
         T.Device([0, 0])
+
+
+def test_wall_budget_on_device_stops_every_system_at_one_barrier(dev):
+    """wall_budget_s: the device stops every system at the first barrier after
+    the budget (no host turn per iteration); the state is exactly the one
+    max_iterations = that many iterations gives (the oracle)."""
+    systems = fixture_systems("sxs")
+    cfg = T.SearchConfig(n_processes=2048, patience=1 << 30, master_seed=6, wall_budget_s=0.02)
+    st = {}
+    res = T.optimize_systems(systems, cfg, [0, 1, 2], stats=st)
+    its = {it for _, it in res}
+    assert len(its) == 1
+    k = its.pop()
+    assert 1 <= k < 1000 and st["graph_launches"] >= k
+    ocfg = T.SearchConfig(n_processes=2048, patience=1 << 30, master_seed=6, max_iterations=k)
+    for c, (sys_, (rec, it)) in enumerate(zip(systems, res)):
+        assert rec_tuple(rec, it) == oracle_tuple(sys_, ocfg, c)[0]
+
+
+def test_wall_budget_rank0_decides_for_every_rank():
+    os.environ["TCSE_SHARED_DEVICES"] = "1"
+    try:
+        d = T.Device([0, 0])
+    finally:
+        os.environ.pop("TCSE_SHARED_DEVICES", None)
+    systems = fixture_systems("laderman")
+    cfg = T.SearchConfig(n_processes=512, patience=1 << 30, master_seed=8, wall_budget_s=0.01)
+    res = T.optimize_systems(systems, cfg, [0, 1, 2], device=d)
+    k = res[0][1]
+    assert all(it == k for _, it in res)
+    ocfg = T.SearchConfig(n_processes=512, patience=1 << 30, master_seed=8, max_iterations=k)
+    for c, (sys_, (rec, it)) in enumerate(zip(systems, res)):
+        assert rec_tuple(rec, it) == oracle_tuple(sys_, ocfg, c)[0]
+    d.close()
+
+
+def test_negative_wall_budget_rejected(dev):
+    with pytest.raises(T.TcseError, match="wall_budget_s"):
+        T.optimize_system(fixture_systems("laderman")[0], T.SearchConfig(wall_budget_s=-1.0))
