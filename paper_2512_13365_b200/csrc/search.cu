@@ -64,6 +64,9 @@ constexpr u64 kMtF = 6364136223846793005ULL;
 #ifndef TCSE_FUSED_TWIST_MIN
 #define TCSE_FUSED_TWIST_MIN 128  // block sizes whose coin generations run register-resident (mt_coin_run)
 #endif
+#ifndef TCSE_COLD_MIN
+#define TCSE_COLD_MIN 64  // block sizes keeping cold per-process values in shared memory
+#endif
 #ifndef TCSE_ONLY_GI
 #define TCSE_ONLY_GI 0
 #endif
@@ -2101,11 +2104,36 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         pre = sd.prefix;
     }
     const bool rec_prefix = reinit != 0;  // records carry the prefix in search mode
-    u32* rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
-    u64* trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
-    const bool dump = sd.mode == kModeDump;
-    int n_rec = 0, step = 0;
+    // cold per-process values (two-warp and wider blocks) live in shared
+    // memory, not in the main loop's registers: the record row and the trace
+    // hook (thread 0 only) and the word-op counter (+3% on 4x4x4, +3% on
+    // 5x5x5; one-warp blocks keep them in registers: -2% there, and so do
+    // 256-thread blocks: -0.5% on 6x6x6).  The slot's alpha / beta / p_greedy
+    // read from shared memory at each use instead: -3% (more spills).
+    constexpr bool kCold = NT >= TCSE_COLD_MIN && NT <= 128;
+    __shared__ u32* s_rec;
+    __shared__ u64* s_trace;
+    __shared__ u64 s_wops;
+    __shared__ int s_step;
+    u32* rec = nullptr;
+    u64* trace = nullptr;
+    int step = 0;
     u64 wops = 0;
+    if (kCold) {
+        if (tid == 0) {
+            s_rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
+            s_trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
+            s_wops = 0;
+            s_step = 0;
+        }
+        __syncthreads();
+    } else {
+        rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
+        trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
+    }
+#define TCSE_REC (kCold ? s_rec : rec)
+    const bool dump = sd.mode == kModeDump;
+    int n_rec = 0;
     // prefix replay (reinit from the incumbent, or a fixed replay): apply +
     // update only, its own loop so the search loop carries no prefix state
     for (int t_pre = 0; t_pre < n_pre; ++t_pre) {
@@ -2123,7 +2151,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         }
         if (rec_prefix) {
             if (tid == 0 && n_rec < sd.sub_cap)
-                rec[n_rec] = q;
+                TCSE_REC[n_rec] = q;
             ++n_rec;
             if (n_rec > sd.sub_cap) {
                 set_error(sd, TCSE_ECAPACITY, n_rec);
@@ -2135,7 +2163,15 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     const int sub_cap = sd.sub_cap;
     const u64 we = u64(sd.words);
     while (!dump) {
-        if (trace) {  // parity hook only
+        if (kCold) {
+            if (s_trace) {  // parity hook only
+                if (tid == 0) {
+                    if (s_step < sd.trace_stride)
+                        s_trace[s_step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
+                    ++s_step;
+                }
+            }
+        } else if (trace) {  // parity hook only
             if (tid == 0 && step < sd.trace_stride)
                 trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
             ++step;
@@ -2172,7 +2208,12 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             sel += mt_ * (Vt - 2) * 4 * we;
         }
         // recount 12(V-1)W_E + substitution 8 W_E + selection
-        wops += 12 * (Vt - 1) * we + 8 * we + sel;
+        if (kCold) {
+            if (tid == 0)
+                s_wops += 12 * (Vt - 1) * we + 8 * we + sel;
+        } else {
+            wops += 12 * (Vt - 1) * we + 8 * we + sel;
+        }
         const u32 q = pr.keys()[pick];
         pr.apply(q);  // a selected candidate always occurs (c >= 2)
         if (!pr.update(q)) {
@@ -2184,9 +2225,12 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             return;
         }
         if (tid == 0)
-            rec[n_rec] = q;
+            TCSE_REC[n_rec] = q;
         ++n_rec;
     }
+    if (kCold)
+        wops = s_wops;
+#undef TCSE_REC
 
     if (dump) {
         if (sd.dump_min_count >= 2) {
