@@ -615,6 +615,7 @@ def optimize_with_flips(scheme, cfg, device=None, stats=None):
     cfg["flip_enabled"] = True
     if cfg["m_schemes"] == 1:
         return optimize_scheme(scheme, cfg, device=device, stats=stats)
+    t0 = time.time()
     d = device or default_device()
     m, n, p, r = scheme["m"], scheme["n"], scheme["p"], scheme["r"]
     flat = lambda t: (C.c_int8 * max(1, sum(len(x) for x in t)))(*[v for row in t for v in row])  # noqa: E731
@@ -647,7 +648,7 @@ def optimize_with_flips(scheme, cfg, device=None, stats=None):
         rec = SolutionRecord.from_c(res.comp[k])
         comps.append(dict(record=rec, cost=rec.cost, naive=res.naive[k], iterations=res.iterations, scheme_id=sid))
     return dict(scheme_digest=scheme_digest(carried), config=resolved, components=comps, total=res.total,
-                iterations=res.iterations, scheme=carried)
+                iterations=res.iterations, scheme=carried, wall_ms=int((time.time() - t0) * 1000))
 
 
 def flip_walk(scheme, rng_seed, flips):

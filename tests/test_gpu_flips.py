@@ -90,3 +90,24 @@ def test_one_scheme_is_optimize_scheme(dev):
     assert flip["total"] == plain["total"]
     for a, b in zip(flip["components"], plain["components"]):
         assert a["record"].substitutions == b["record"].substitutions
+
+
+def test_cli_flip_mode_writes_the_reference_report(tmp_path):
+    """`tcse_cli.py reduce --flip-mode --flip-schemes M` dispatches to flip
+    mode (terncse_cli.cpp:85-86, 163-164) and writes the reference's report."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "s.json"
+    src.write_text(open(os.path.join(SCHEMES, "laderman.json")).read())
+    out = tmp_path / "r.json"
+    cmd = [sys.executable, os.path.join(root, "tools", "tcse_cli.py"), "reduce", str(src), "--flip-mode",
+           "--flip-schemes", "4", "--processes", "32", "--iterations-patience", "2", "--seed", "5",
+           "--out-report", str(out)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    cfg = T.SearchConfig(n_processes=32, patience=2, master_seed=5, m_schemes=4)
+    assert out.read_text() == ref_flip_report(src.read_text(), cfg)
+    # the report round-trips and names the carried scheme's variant
+    rep = T.parse_report(out.read_text())
+    assert rep["config"]["flip_enabled"] and all("scheme_id" in c for c in rep["components"])
