@@ -248,7 +248,7 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
     const u32 NW = u32(nt / 32);
     const u32 vc = u32(vcap), mc = u32(mcap);
     u32 o = 0;
-    L->mask = o;
+    L->mask = o;  // must stay 0: search.cu mask_base() relies on it
     o += al16(vc * 2u * u32(W) * 8u);
     // one candidate list: the update copies the old keys into its scratch
     // (kcopy) and rewrites the list in place

@@ -132,6 +132,10 @@ __device__ __forceinline__ u64 globaltimer() {
     return t;
 }
 
+// the masks open the carve (carve(): offset 0), so their base needs no
+// load of the layout from shared memory
+__device__ __forceinline__ u64* mask_base() { return reinterpret_cast<u64*>(g_smem); }
+
 template <typename T>
 __device__ __forceinline__ T* sp(u32 off) {
     return reinterpret_cast<T*>(g_smem + off);
@@ -642,8 +646,8 @@ __device__ __noinline__ void derive_slot(const SysDesc& sd, int iteration, u64 p
 // frequency of (a, b, neg), 1-based ids (count_pairs, linear_system.hpp:151-161)
 template <int W>
 __device__ __forceinline__ int count_pair(int a, int b, int neg) {
-    const u64* pa = sp<u64>(lay.mask) + size_t(a - 1) * 2 * W;
-    const u64* pb = sp<u64>(lay.mask) + size_t(b - 1) * 2 * W;
+    const u64* pa = mask_base() + size_t(a - 1) * 2 * W;
+    const u64* pb = mask_base() + size_t(b - 1) * 2 * W;
     int c = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w)
@@ -720,8 +724,8 @@ struct St {
 
     __device__ __forceinline__ u32* keys() { return sp<u32>(lay.keys0); }
     __device__ __forceinline__ u16* cnts() { return sp<u16>(lay.cnts0); }
-    __device__ __forceinline__ u64* P(int v) { return sp<u64>(lay.mask) + size_t(v) * 2 * W; }
-    __device__ __forceinline__ u64* N(int v) { return sp<u64>(lay.mask) + size_t(v) * 2 * W + W; }
+    __device__ __forceinline__ u64* P(int v) { return mask_base() + size_t(v) * 2 * W; }
+    __device__ __forceinline__ u64* N(int v) { return mask_base() + size_t(v) * 2 * W + W; }
     __device__ __forceinline__ u32* red() {
         rsel ^= 1;
         return sp<u32>(lay.red) + rsel * (NW + 2);
@@ -2025,7 +2029,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     }
     __syncthreads();
     {
-        u64* mask = sp<u64>(lay.mask);
+        u64* mask = mask_base();
         const int nw = sd.n_x * 2 * W;
         for (int t = tid; t < nw; t += NT)
             mask[t] = sd.base_masks[t];
