@@ -2029,16 +2029,25 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     }
     __syncthreads();
     {
+        // (descriptor fields in registers first: read through the descriptor
+        // reference, every iteration would reload them behind the shared
+        // stores, serialising the copy on the load latency)
         u64* mask = mask_base();
         const int nw = sd.n_x * 2 * W;
+        const u64* __restrict__ gmask = sd.base_masks;
+#pragma unroll 4
         for (int t = tid; t < nw; t += NT)
-            mask[t] = sd.base_masks[t];
-        if (sd.base_keys) {
+            mask[t] = __ldg(gmask + t);
+        const u32* __restrict__ gkeys = sd.base_keys;
+        const u16* __restrict__ gcnts = sd.base_cnts;
+        const int bm = sd.base_m;
+        if (gkeys) {
             u32* k0 = sp<u32>(lay.keys0);
             u16* c0 = sp<u16>(lay.cnts0);
-            for (int t = tid; t < sd.base_m; t += NT) {
-                k0[t] = sd.base_keys[t];
-                c0[t] = sd.base_cnts[t];
+#pragma unroll 4
+            for (int t = tid; t < bm; t += NT) {
+                k0[t] = __ldg(gkeys + t);
+                c0[t] = __ldg(gcnts + t);
             }
         }
         if (s_slot.rng && !L.rng) {
