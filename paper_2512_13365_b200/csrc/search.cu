@@ -1118,15 +1118,27 @@ struct St {
         // second element, B = as first element)
         if (!walk) {
             u32 lmax = 0u;
+            // bitmap layout: row 0 (no variable has id 0) marks the heavy
+            // candidates (c >= 3, weight > 1), one ballot per 32 of them
+            const bool hb = approx && gi_bm;
+            const int mr = hb ? (m + 31) & ~31 : m;
 #pragma unroll 1
-            for (int t = tid; t < m; t += NT) {
-                const u32 kk = ks[t];
-                atomicAdd(&nA[key_i(kk)], 1u);
-                atomicAdd(&nA[key_j(kk)], 1u);
-                lmax = max(lmax, u32(c[t]) - 1u);
-                if (approx && gi_bm) {
-                    atomicOr(&bm[key_i(kk) * nwl + (t >> 5)], 1u << (t & 31));
-                    atomicOr(&bm[key_j(kk) * nwl + (t >> 5)], 1u << (t & 31));
+            for (int t = tid; t < mr; t += NT) {
+                const bool on = t < m;
+                if (on) {
+                    const u32 kk = ks[t];
+                    atomicAdd(&nA[key_i(kk)], 1u);
+                    atomicAdd(&nA[key_j(kk)], 1u);
+                    lmax = max(lmax, u32(c[t]) - 1u);
+                    if (hb) {
+                        atomicOr(&bm[key_i(kk) * nwl + (t >> 5)], 1u << (t & 31));
+                        atomicOr(&bm[key_j(kk) * nwl + (t >> 5)], 1u << (t & 31));
+                    }
+                }
+                if (hb) {  // warp-uniform: mr and NT are multiples of 32
+                    const u32 heavy = __ballot_sync(FULLMASK, on && c[t] >= 3);
+                    if (lane == 0)
+                        bm[t >> 5] = heavy;
                 }
             }
             if (approx) {
@@ -1559,27 +1571,39 @@ struct St {
         const int nwl = int(bm_stride(mcap));
         const u32* bi = sp<u32>(lay.bm) + key_i(kq) * nwl;
         const u32* bj = sp<u32>(lay.bm) + key_j(kq) * nwl;
+        const u32* hv0 = sp<u32>(lay.bm);  // row 0: heavy candidates (c >= 3)
         const u32 p = sp<u32>(lay.qbase)[q] - c0;
         const u32 w0 = coin[p >> 5], w1 = coin[(p >> 5) + 1], w2 = coin[(p >> 5) + 2];
-        u32 lo = __funnelshift_r(w0, w1, p & 31u), hi = __funnelshift_r(w1, w2, p & 31u);
-        u32 A = 0u;
+        // q's coins: bit k decides its k-th intersecting candidate
+        u64 win = (u64(__funnelshift_r(w1, w2, p & 31u)) << 32) | __funnelshift_r(w0, w1, p & 31u);
+        // per word of the list: the n intersecting candidates there take the
+        // window's next n coins; weight-1 candidates (c = 2, the common
+        // case) count by popcount, only heavy ones are visited one by one
+        u32 I = 0u, C = 0u;
         const int nwm = (m + 31) >> 5;
 #pragma unroll 1
         for (int wd = 0; wd < nwm; ++wd) {
             u32 msk = bi[wd] | bj[wd];
             if (wd == (q >> 5))
                 msk &= ~(1u << (q & 31));
-            while (msk) {
-                const int s = (wd << 5) + __ffs(msk) - 1;
-                msk &= msk - 1;
-                const u32 w = u32(c[s]) - 1u;
-                A += (w << 16) + ((lo & 1u) ? w : 0u);
-                lo = __funnelshift_r(lo, hi, 1);
-                hi >>= 1;
+            if (msk == 0u)
+                continue;
+            const int n = __popc(msk);
+            const u32 sel = u32(win) & (0xffffffffu >> (32 - n));  // coins of these n, in order
+            I += u32(n);
+            C += u32(__popc(sel));
+            u32 hv = msk & hv0[wd];
+            while (hv) {
+                const int b = __ffs(hv) - 1;
+                hv &= hv - 1;
+                const u32 x = u32(c[(wd << 5) + b]) - 2u;  // weight beyond 1
+                I += x;
+                C += ((sel >> __popc(msk & ((1u << b) - 1u))) & 1u) ? x : 0u;
             }
+            win >>= n;
         }
         const u32 wq = u32(c[q]) - 1u;
-        const double F = __dadd_rn(double(T - wq - (A >> 16)), __dmul_rn(beta, double(A & 0xffffu)));
+        const double F = __dadd_rn(double(T - wq - I), __dmul_rn(beta, double(C)));
         const double h = __dadd_rn(double(wq), __dmul_rn(alpha, F));
         lb = fmax(lb, h);
         const double lim = __dsub_rn(lb, eps2);
