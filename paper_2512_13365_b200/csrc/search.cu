@@ -78,6 +78,12 @@ constexpr u64 kMtF = 6364136223846793005ULL;
 #endif
 constexpr u64 kCoinMask = 0x8080000004000200ULL;
 
+// coin of raw state word x: parity of x & kCoinMask (one POPC: the two
+// halves' masked bits folded by XOR first)
+__device__ __forceinline__ u32 coin_bit(u64 x) {
+    return u32(__popc((u32(x >> 32) & u32(kCoinMask >> 32)) ^ (u32(x) & u32(kCoinMask)))) & 1u;
+}
+
 __device__ __forceinline__ u64 mt_temper(u64 z) {
     z ^= (z >> 29) & 0x5555555555555555ULL;
     z ^= (z << 17) & 0x71d67fffeda60000ULL;
@@ -334,7 +340,7 @@ __device__ __noinline__ void mt_twist_impl(u32* coin, u32 pos0, u32 n) {
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const int e = i + half * 156;
-                const u32 bit = (i < 156 && u32(e) < n) ? (u32(__popcll((half ? hi[r] : lo[r]) & kCoinMask)) & 1u) : 0u;
+                const u32 bit = (i < 156 && u32(e) < n) ? coin_bit(half ? hi[r] : lo[r]) : 0u;
                 const u32 ball = __ballot_sync(FULLMASK, bit);
                 if (lane == 0 && ball) {
                     const u32 pos = pos0 + u32(e);
@@ -402,7 +408,7 @@ __device__ __noinline__ void mt_twist_small() {
 // by one ballot, straight from the registers the twist computed them in: no
 // second pass over the state in shared memory)
 __device__ __forceinline__ void coin_ballot(u32* coin, u32 pos0, int e, u32 n, u64 x, int lane) {
-    const u32 bit = u32(e) < n ? (u32(__popcll(x & kCoinMask)) & 1u) : 0u;
+    const u32 bit = u32(e) < n ? coin_bit(x) : 0u;
     const u32 ball = __ballot_sync(FULLMASK, bit);
     if (lane == 0 && ball) {
         const u32 pos = pos0 + u32(e - lane);
@@ -522,8 +528,8 @@ __device__ __noinline__ u32 mt_coin_run(u32* coin, u32 pos0, u32 nbits) {
             lo[r] = l2;
             hi[r] = h2;
             const bool ok = i < 156;
-            const u32 blo = (ok && u32(i) < n_t) ? (u32(__popcll(l2 & kCoinMask)) & 1u) : 0u;
-            const u32 bhi = (ok && u32(i) + 156u < n_t) ? (u32(__popcll(h2 & kCoinMask)) & 1u) : 0u;
+            const u32 blo = (ok && u32(i) < n_t) ? coin_bit(l2) : 0u;
+            const u32 bhi = (ok && u32(i) + 156u < n_t) ? coin_bit(h2) : 0u;
             const u32 balo = __ballot_sync(FULLMASK, blo);
             const u32 bahi = __ballot_sync(FULLMASK, bhi);
             if (lane == 0) {
@@ -764,9 +770,11 @@ struct St {
 
     // n coin flips (uniform_int_distribution<int>(0,1) == top tempered bit)
     // precleared: the caller zeroed the buffer's first words behind a barrier
+    // (only the register-resident generations of 128-/256-thread blocks OR
+    // bits into the buffer; smaller blocks store whole words)
     __device__ void draw_coins(u32 nbits, bool precleared = false) {
         u32* coin = sp<u32>(lay.coin);
-        if (!precleared) {
+        if (!precleared && (NT >= TCSE_FUSED_TWIST_MIN || TCSE_SMALL_TWIST_COINS)) {
             const u32 words = (nbits + 31) >> 5;
 #pragma unroll 1
             for (u32 w = tid; w < words; w += NT)
@@ -795,18 +803,26 @@ struct St {
 #endif
                 }
             }
+            // this segment's coins as whole buffer words: lane l of word k
+            // holds position 32 (done / 32 + k) + l, element l + 32 k - sh of
+            // the generation's remaining outputs; a plain store per word,
+            // except the first word's OR onto the previous segment's bits
+            // (written before the twist's barriers).  Bits past the segment
+            // stay zero until the next segment ORs them.
             const u32 n = min(u32(312 - mti), nbits - done);
-            const u32 n32 = (n + 31) & ~31u;
+            const u32 sh = done & 31u;
+            const u32 nw32 = (sh + n + 31) & ~31u;
             const u64* mt = sp<u64>(lay.mt) + mti;
-            for (u32 e = tid; e < n32; e += NT) {
-                const u32 bit = e < n ? (u32(__popcll(mt[e] & kCoinMask)) & 1u) : 0u;
+            u32* cw = coin + (done >> 5);
+            for (u32 t = tid; t < nw32; t += NT) {
+                const u32 e = t - sh;  // wraps for t < sh: out of range
+                const u32 bit = e < n ? coin_bit(mt[e]) : 0u;
                 const u32 ball = __ballot_sync(FULLMASK, bit);
-                if (lane == 0 && ball) {
-                    const u32 pos = done + e;
-                    const u32 w0 = pos >> 5, sh = pos & 31;
-                    atomicOr(&coin[w0], ball << sh);
-                    if (sh)
-                        atomicOr(&coin[w0 + 1], ball >> (32 - sh));
+                if (lane == 0) {
+                    if (t < 32u && sh)
+                        cw[0] |= ball;
+                    else
+                        cw[t >> 5] = ball;
                 }
             }
             mti += int(n);
@@ -1247,7 +1263,9 @@ struct St {
                 if (walk || approx)
                     wp[m] = W_;
             }
-            if (dense) {  // the first coin chunk's words, behind the barrier below
+            // the first coin chunk's words, behind the barrier below (only
+            // where coin bits are OR-ed in: draw_coins)
+            if (dense && (NT >= TCSE_FUSED_TWIST_MIN || TCSE_SMALL_TWIST_COINS)) {
                 u32* coin = sp<u32>(lay.coin);
                 const u32 words = (min(D, lay.coin_cap) + 31) >> 5;
 #pragma unroll 1
