@@ -121,6 +121,14 @@ struct SysDesc {
     // session: iteration, incumbent length and the active flag come from the
     // device loop state instead of iteration / inc_len (null: host-driven)
     const IncState* loop;
+    // prefix snapshots (session search mode, else null): the state after k
+    // substitutions of the incumbent, k = 1..snap_k, published by the
+    // launch's builder block as it replays (snap_ready = newest k, reset by
+    // the prep kernel); snapshot k at snap + (k - 1) * snap_stride:
+    // [V, m, cost, 0] | masks u64[V][2W] | keys u32 at snap_koff | cnts u16 at snap_coff
+    unsigned char* snap;
+    u32* snap_ready;
+    int32_t snap_k, snap_stride, snap_koff, snap_coff;
     const u32* prefix;  // fixed prefix (run / dump modes)
     int32_t prefix_len;
 
@@ -166,6 +174,7 @@ struct LaunchDesc {
     const SysDesc* table;  // > kMaxSys systems (flip mode): device table, blocks contiguous per system
     int32_t table_n;
     int32_t group;         // launch group index (clock stamps)
+    int32_t n_builders;    // blocks 0..n_builders-1 build sys[b]'s prefix snapshots; processes follow
     LoopClock* clock;      // or null
     SysDesc sys[kMaxSys];
 };

@@ -2052,11 +2052,158 @@ struct MinBlocks {
     static constexpr int value = NT == 32 ? TCSE_MINB32 : (NT == 64 ? TCSE_MINB64 : (NT == 128 ? 8 : 4));
 };
 
+// ------------------------------------------------------ prefix snapshots
+//
+// A reinit process (parallel_search.hpp:242-248) replays the first k
+// substitutions of the incumbent, k ~ U[1, 3 len / 4]; every such process of
+// an iteration replays a prefix of the SAME record.  The launch's builder
+// block (one per system, scheduled first) replays it once with the same
+// apply / update code and publishes the state after each substitution; a
+// reinit process copies the newest published state at or below its k from
+// L2 and replays only the rest — the same state either way, so results do
+// not depend on how far the builder got (nobody waits for it).
+
+__device__ __forceinline__ u32 ld_acquire(const u32* p) {
+    u32 v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(u32* p, u32 v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// the system's base state (masks of the n_x input variables, starting
+// candidate list) into shared memory
+template <int W, int NT>
+__device__ __forceinline__ void load_base(const SysDesc& sd, int tid) {
+    // (descriptor fields in registers first: read through the descriptor
+    // reference, every iteration would reload them behind the shared
+    // stores, serialising the copy on the load latency)
+    u64* mask = mask_base();
+    const int nw = sd.n_x * 2 * W;
+    const u64* __restrict__ gmask = sd.base_masks;
+#pragma unroll 4
+    for (int t = tid; t < nw; t += NT)
+        mask[t] = __ldg(gmask + t);
+    const u32* __restrict__ gkeys = sd.base_keys;
+    const u16* __restrict__ gcnts = sd.base_cnts;
+    const int bm = sd.base_m;
+    if (gkeys) {
+        u32* k0 = sp<u32>(lay.keys0);
+        u16* c0 = sp<u16>(lay.cnts0);
+#pragma unroll 4
+        for (int t = tid; t < bm; t += NT) {
+            k0[t] = __ldg(gkeys + t);
+            c0[t] = __ldg(gcnts + t);
+        }
+    }
+}
+
+// snapshot k (1-based) of the state in shared memory: (V, m, cost) header,
+// V mask rows, the list
+template <int W, int NT>
+__device__ __noinline__ void snap_store(const SysDesc& sd, int k, int V, int m, int cost) {
+    const int tid = threadIdx.x;
+    unsigned char* base = sd.snap + size_t(k - 1) * size_t(sd.snap_stride);
+    if (tid == 0)
+        *reinterpret_cast<int4*>(base) = make_int4(V, m, cost, 0);
+    const u64* mask = mask_base();
+    u64* gm = reinterpret_cast<u64*>(base + 16);
+    for (int t = tid; t < V * 2 * W; t += NT)
+        gm[t] = mask[t];
+    const u32* ks = sp<u32>(lay.keys0);
+    const u16* cs = sp<u16>(lay.cnts0);
+    u32* gk = reinterpret_cast<u32*>(base + sd.snap_koff);
+    u16* gc = reinterpret_cast<u16*>(base + sd.snap_coff);
+    for (int t = tid; t < m; t += NT) {
+        gk[t] = ks[t];
+        gc[t] = cs[t];
+    }
+}
+
+// snapshot k into shared memory (L2 reads: the lines may be stale in L1
+// from an earlier iteration); returns (V, m, cost)
+template <int W, int NT>
+__device__ __noinline__ int4 snap_load(const SysDesc& sd, int k) {
+    const int tid = threadIdx.x;
+    const unsigned char* base = sd.snap + size_t(k - 1) * size_t(sd.snap_stride);
+    const int4 h = __ldcg(reinterpret_cast<const int4*>(base));
+    u64* mask = mask_base();
+    const u64* gm = reinterpret_cast<const u64*>(base + 16);
+    for (int t = tid; t < h.x * 2 * W; t += NT)
+        mask[t] = __ldcg(gm + t);
+    u32* ks = sp<u32>(lay.keys0);
+    u16* cs = sp<u16>(lay.cnts0);
+    const u32* gk = reinterpret_cast<const u32*>(base + sd.snap_koff);
+    const u16* gc = reinterpret_cast<const u16*>(base + sd.snap_coff);
+    for (int t = tid; t < h.y; t += NT) {
+        ks[t] = __ldcg(gk + t);
+        cs[t] = __ldcg(gc + t);
+    }
+    return h;
+}
+
+template <int W, int NT>
+struct St;
+
+// the builder block of sys: replays the incumbent's first 3 len / 4
+// substitutions (the longest prefix a reinit process draws) and publishes
+// each state.  Same conditions as prep_slot's reinit flag; a prefix the
+// processes could not replay (capacity, bad pair) is simply not published —
+// the processes replay it themselves and report exactly as without snapshots.
+template <int W, int NT>
+__device__ __noinline__ void build_snapshots(const SysDesc& sd) {
+    const int tid = threadIdx.x;
+    const IncState* I = sd.loop;
+    if (!sd.snap || !I || !sd.reinit || !I->active || *sd.err != 0)
+        return;
+    const int len = I->len;
+    const int K = min(3 * len / 4, sd.snap_k);
+    if (len < 2 || K < 1)
+        return;
+    if (tid == 0)
+        carve(&lay, W, NT, sd.vcap, sd.mcap, sd.n_e, sd.coin_words, sd.gi_dense, sd.gi_bm);
+    __syncthreads();
+    load_base<W, NT>(sd, tid);
+    __syncthreads();
+    St<W, NT> pr;
+    pr.tid = tid;
+    pr.lane = tid & 31;
+    pr.V = sd.n_x;
+    pr.cost = sd.naive;
+    pr.m = sd.base_m;
+    pr.mti = 312;
+    pr.rsel = 0;
+    pr.last_coins = 0;
+    pr.sd_ne = sd.n_e;
+    pr.gi_prune = sd.gi_prune;
+    pr.gi_bm = sd.gi_bm;
+    pr.mcap = sd.mcap;
+    for (int k = 1; k <= K; ++k) {
+        const u32 q = sd.inc_keys[k - 1];
+        const int qi = key_i(q), qj = key_j(q);
+        if (qi < 1 || qj <= qi || qj > pr.V || pr.apply(q) == 0 || !pr.update(q))
+            return;
+        snap_store<W, NT>(sd, k, pr.V, pr.m, pr.cost);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release(sd.snap_ready, u32(k));
+        }
+    }
+}
+
 template <int W, int NT, bool GID>
 __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const __grid_constant__ LaunchDesc L) {
+    if (int(blockIdx.x) < L.n_builders) {
+        build_snapshots<W, NT>(L.sys[blockIdx.x]);
+        return;
+    }
     // launch order -> process block: blocks of one strategy run together, most
     // expensive strategies first (instruction-cache locality, shorter tail)
-    const int blk = L.perm ? L.perm[blockIdx.x] : int(blockIdx.x);
+    const int bx = int(blockIdx.x) - L.n_builders;
+    const int blk = L.perm ? L.perm[bx] : bx;
     const SysDesc& sd = find_sys(L, blk);
     const int lp = blk - sd.block_begin;
     if (lp >= sd.n_local)
@@ -2070,28 +2217,12 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         s_slot = L.slots[blk];
     }
     __syncthreads();
+    // a reinit process with snapshots loads its state once it knows its
+    // prefix length (below)
+    const bool snap = sd.snap && sd.base_keys && s_slot.reinit;
     {
-        // (descriptor fields in registers first: read through the descriptor
-        // reference, every iteration would reload them behind the shared
-        // stores, serialising the copy on the load latency)
-        u64* mask = mask_base();
-        const int nw = sd.n_x * 2 * W;
-        const u64* __restrict__ gmask = sd.base_masks;
-#pragma unroll 4
-        for (int t = tid; t < nw; t += NT)
-            mask[t] = __ldg(gmask + t);
-        const u32* __restrict__ gkeys = sd.base_keys;
-        const u16* __restrict__ gcnts = sd.base_cnts;
-        const int bm = sd.base_m;
-        if (gkeys) {
-            u32* k0 = sp<u32>(lay.keys0);
-            u16* c0 = sp<u16>(lay.cnts0);
-#pragma unroll 4
-            for (int t = tid; t < bm; t += NT) {
-                k0[t] = __ldg(gkeys + t);
-                c0[t] = __ldg(gcnts + t);
-            }
-        }
+        if (!snap)
+            load_base<W, NT>(sd, tid);
         if (s_slot.rng && !L.rng) {
             // seed the process's mt19937_64 in shared memory (one thread, while
             // the others load the base state): no HBM hand-off
@@ -2189,9 +2320,31 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
 #define TCSE_REC (kCold ? s_rec : rec)
     const bool dump = sd.mode == kModeDump;
     int n_rec = 0;
+    int t_pre0 = 0;
+    if (snap) {
+        // the newest published snapshot at or below n_pre (or the base state)
+        __shared__ int s_k;
+        if (tid == 0)
+            s_k = min(n_pre, int(ld_acquire(sd.snap_ready)));
+        __syncthreads();
+        t_pre0 = s_k;
+        if (t_pre0 > 0) {
+            const int4 h = snap_load<W, NT>(sd, t_pre0);
+            pr.V = h.x;
+            pr.m = h.y;
+            pr.cost = h.z;
+            if (sd.out_subs)  // the record carries the prefix
+                for (int t = tid; t < t_pre0; t += NT)
+                    TCSE_REC[t] = pre[t];
+            n_rec = t_pre0;
+        } else {
+            load_base<W, NT>(sd, tid);
+        }
+        __syncthreads();
+    }
     // prefix replay (reinit from the incumbent, or a fixed replay): apply +
     // update only, its own loop so the search loop carries no prefix state
-    for (int t_pre = 0; t_pre < n_pre; ++t_pre) {
+    for (int t_pre = t_pre0; t_pre < n_pre; ++t_pre) {
         const u32 q = pre[t_pre];
         const int qi = key_i(q), qj = key_j(q);
         if (qi < 1 || qj <= qi || qj > pr.V || pr.apply(q) == 0) {
@@ -2423,6 +2576,8 @@ __global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ L
     const int tid = threadIdx.x;
     if (b == 0 && L.clock && L.group == 0 && L.clock->t_begin == 0)
         L.clock->t_begin = globaltimer();  // the search's first launch
+    if (b < L.nsys && L.sys[b].snap_ready)
+        *L.sys[b].snap_ready = 0u;  // no snapshot of this iteration yet (search launch follows on the stream)
     const PrepOut o = prep_slot(L, b);
     u64 x0 = 0, x1 = 0, x156 = 0;  // for the first output (work class below)
     if (L.rng) {
@@ -3031,7 +3186,7 @@ static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess)
         return e;
-    k<<<L.total_blocks, NT, smem, st>>>(L);
+    k<<<L.total_blocks + L.n_builders, NT, smem, st>>>(L);
     return cudaGetLastError();
 }
 
