@@ -120,13 +120,21 @@ __device__ __forceinline__ double uniform_real(u64 x, double a, double b) {
 
 __shared__ Lay lay;
 
-#ifdef TCSE_GI_STATS
+#if defined(TCSE_GI_STATS) || defined(TCSE_SNAP_STATS)
 // debug build only: gi path counters (approx steps, lone picks, folds,
 // overflow fallbacks, reference-loop steps, sum of m, multi-survivor steps)
 __device__ unsigned long long g_gi_stats[8];
-#define GI_STAT(k, v) do { if (threadIdx.x == 0) atomicAdd(&g_gi_stats[k], (unsigned long long)(v)); } while (0)
+#define DBG_STAT(k, v) do { if (threadIdx.x == 0) atomicAdd(&g_gi_stats[k], (unsigned long long)(v)); } while (0)
+#endif
+#ifdef TCSE_GI_STATS
+#define GI_STAT(k, v) DBG_STAT(k, v)
 #else
 #define GI_STAT(k, v) do { } while (0)
+#endif
+#ifdef TCSE_SNAP_STATS  // snapshot use: reinit processes, full hits, misses, sum of prefixes, steps replayed anyway
+#define SNAP_STAT(k, v) DBG_STAT(k, v)
+#else
+#define SNAP_STAT(k, v) do { } while (0)
 #endif
 
 __device__ __forceinline__ double __int_as_double_lo(int v) { return __hiloint2double(0, v); }
@@ -2076,7 +2084,7 @@ __device__ __forceinline__ void st_release(u32* p, u32 v) {
 // the system's base state (masks of the n_x input variables, starting
 // candidate list) into shared memory
 template <int W, int NT>
-__device__ __forceinline__ void load_base(const SysDesc& sd, int tid) {
+__device__ __forceinline__ void load_base_impl(const SysDesc& sd, int tid) {
     // (descriptor fields in registers first: read through the descriptor
     // reference, every iteration would reload them behind the shared
     // stores, serialising the copy on the load latency)
@@ -2098,6 +2106,21 @@ __device__ __forceinline__ void load_base(const SysDesc& sd, int tid) {
             c0[t] = __ldg(gcnts + t);
         }
     }
+}
+
+// one out-of-line copy for two-warp and wider blocks (fewer spills in the
+// main loop: +1% on 4x4x4); one-warp blocks inline it (-1% out of line)
+template <int W, int NT>
+__device__ __noinline__ void load_base_ool(const SysDesc& sd, int tid) {
+    load_base_impl<W, NT>(sd, tid);
+}
+
+template <int W, int NT>
+__device__ __forceinline__ void load_base(const SysDesc& sd, int tid) {
+    if constexpr (NT >= 64)
+        load_base_ool<W, NT>(sd, tid);
+    else
+        load_base_impl<W, NT>(sd, tid);
 }
 
 // snapshot k (1-based) of the state in shared memory: (V, m, cost) header,
@@ -2328,6 +2351,11 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             s_k = min(n_pre, int(ld_acquire(sd.snap_ready)));
         __syncthreads();
         t_pre0 = s_k;
+        SNAP_STAT(0, 1);
+        SNAP_STAT(1, t_pre0 == n_pre);
+        SNAP_STAT(2, t_pre0 == 0);
+        SNAP_STAT(3, n_pre);
+        SNAP_STAT(4, n_pre - t_pre0);
         if (t_pre0 > 0) {
             const int4 h = snap_load<W, NT>(sd, t_pre0);
             pr.V = h.x;
@@ -3251,7 +3279,7 @@ int search_smem_attr_max() { return 227 * 1024; }
 
 }  // namespace tcse
 
-#ifdef TCSE_GI_STATS
+#if defined(TCSE_GI_STATS) || defined(TCSE_SNAP_STATS)
 extern "C" int tcse_debug_gi_stats(unsigned long long* out, int reset) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, tcse::g_gi_stats, sizeof(unsigned long long) * 8);
