@@ -968,7 +968,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     rc = base_candidates(ctx, d);
     if (rc)
         return rc;
-    DBuf dpre, dcfg, dcost, dlen, down, dstrat, dseed, dsubs, dtrace;
+    DBuf dpre, dcfg, dcost, dlen, down, dstrat, dseed, dwops, dsubs, dtrace;
     rc = upload_pairs(ctx, prefix, n_prefix, &dpre);
     if (rc)
         return rc;
@@ -980,6 +980,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     CU(down.reserve(4 * size_t(n)));
     CU(dstrat.reserve(4 * size_t(n)));
     CU(dseed.reserve(8 * size_t(n)));
+    CU(dwops.reserve(8 * size_t(n)));
     CU(dsubs.reserve(4 * size_t(n) * size_t(sub_cap)));
     if (trace && trace_stride > 0)
         CU(dtrace.reserve(8 * size_t(n) * size_t(trace_stride)));
@@ -1003,6 +1004,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
     sd.out_own = down.as<int32_t>();
     sd.out_strategy = dstrat.as<int32_t>();
     sd.out_seed = dseed.as<u64>();
+    sd.out_wops = dwops.as<u64>();
     sd.out_subs = dsubs.as<u32>();
     sd.trace = (trace && trace_stride > 0) ? dtrace.as<u64>() : nullptr;
     sd.trace_stride = trace_stride;
@@ -1020,20 +1022,22 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
         return rc;
     const size_t nn = size_t(n);
     std::vector<int32_t> hcost(nn), hlen(nn), hown(nn), hstrat(nn);
-    std::vector<u64> hseed((size_t)n);
+    std::vector<u64> hseed((size_t)n), hwops((size_t)n);
     std::vector<u32> hsubs(size_t(n) * size_t(sub_cap));
     CU(cudaMemcpyAsync(hcost.data(), dcost.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hlen.data(), dlen.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hown.data(), down.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hstrat.data(), dstrat.p, 4 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hseed.data(), dseed.p, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hwops.data(), dwops.p, 8 * size_t(n), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hsubs.data(), dsubs.p, 4 * size_t(n) * size_t(sub_cap), cudaMemcpyDeviceToHost, ctx->stream));
     if (sd.trace)
         CU(cudaMemcpyAsync(trace, dtrace.p, 8 * size_t(n) * size_t(trace_stride), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    uint64_t steps = 0;
+    uint64_t steps = 0, wops = 0;
     for (int b = 0; b < n; ++b) {
         tcse_record& r = out[b];
+        wops += hwops[size_t(b)];
         if (hlen[size_t(b)] > r.cap)
             return fail(TCSE_ECAPACITY, "run_cse: record %d needs %d entries, capacity %d", b, hlen[size_t(b)], r.cap);
         for (int t = 0; t < hlen[size_t(b)]; ++t)
@@ -1050,6 +1054,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         stats->kernel_ms = ms;
         stats->steps = steps;
+        stats->wops = wops;
         stats->processes = uint64_t(n);
         stats->launches = 1;
         stats->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

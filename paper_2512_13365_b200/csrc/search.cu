@@ -2315,30 +2315,26 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     const bool rec_prefix = reinit != 0;  // records carry the prefix in search mode
     // cold per-process values (two-warp and wider blocks) live in shared
     // memory, not in the main loop's registers: the record row and the trace
-    // hook (thread 0 only) and the word-op counter (+3% on 4x4x4, +3% on
+    // hook (thread 0 only; round 2 also took the word-op counter there: +3% on 4x4x4, +3% on
     // 5x5x5; one-warp blocks keep them in registers: -2% there, and so do
     // 256-thread blocks: -0.5% on 6x6x6).  The slot's alpha / beta / p_greedy
     // read from shared memory at each use instead: -3% (more spills).
     constexpr bool kCold = NT >= TCSE_COLD_MIN && NT <= 128;
     __shared__ u32* s_rec;
     __shared__ u64* s_trace;
-    __shared__ u64 s_wops;
     __shared__ int s_step;
     u32* rec = nullptr;
-    u64* trace = nullptr;
     int step = 0;
     u64 wops = 0;
     if (kCold) {
         if (tid == 0) {
             s_rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
             s_trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
-            s_wops = 0;
             s_step = 0;
         }
         __syncthreads();
     } else {
         rec = sd.out_subs ? sd.out_subs + size_t(lp) * size_t(sd.sub_cap) : nullptr;
-        trace = sd.trace ? sd.trace + size_t(lp) * size_t(sd.trace_stride) : nullptr;
     }
 #define TCSE_REC (kCold ? s_rec : rec)
     const bool dump = sd.mode == kModeDump;
@@ -2397,19 +2393,27 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
     }
     const int n_rec0 = n_rec;  // steps selected by this process = n_rec - n_rec0
     const int sub_cap = sd.sub_cap;
-    const u64 we = u64(sd.words);
+    const int V0 = pr.V;  // V grows by one per selected step
+    // word-ops per step: recount 12 (V - 1) W_E +
+    // substitution 8 W_E + selection (m, + coins for gi, + m (V - 2) 4 W_E
+    // for gp); the V terms are summed in closed form after the loop, the
+    // list sizes and coins here, gp's rare term in shared memory
+    u32 msum = 0;
+    __shared__ u64 s_gpw;
+    if (tid == 0)
+        s_gpw = 0;
     while (!dump) {
         if (kCold) {
-            if (s_trace) {  // parity hook only
+            if (sd.trace) {  // parity hook only
                 if (tid == 0) {
                     if (s_step < sd.trace_stride)
                         s_trace[s_step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
                     ++s_step;
                 }
             }
-        } else if (trace) {  // parity hook only
+        } else if (sd.trace) {  // parity hook only
             if (tid == 0 && step < sd.trace_stride)
-                trace[step] = cand_hash(pr.keys(), pr.cnts(), pr.m);
+                sd.trace[size_t(lp) * size_t(sd.trace_stride) + size_t(step)] = cand_hash(pr.keys(), pr.cnts(), pr.m);
             ++step;
         }
         if (pr.m == 0)
@@ -2421,13 +2425,12 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             strat = uniform_real(pr.draw(), 0.0, 1.0) < p_greedy ? TCSE_GREEDY_ALTERNATIVE : TCSE_WEIGHTED_RANDOM;
         if ((strat == TCSE_GREEDY_INTERSECTIONS || strat == TCSE_GREEDY_POTENTIAL) && alpha == 0.0)
             strat = TCSE_GREEDY;  // gain only (strategies.hpp:140-141, 205-206)
-        const u64 Vt = u64(pr.V), mt_ = u64(pr.m);
+        msum += u32(pr.m);
         int pick;
-        u64 sel = mt_;
 #if TCSE_ONLY_GI  // experiment: a Greedy-Intersections-only kernel (code size / registers)
         if (true) {
             pick = pr.template sel_gi<GID>(alpha, beta);
-            sel += pr.last_coins;
+            msum += pr.last_coins;
         } else
 #endif
         if (strat == TCSE_GREEDY) {
@@ -2438,17 +2441,11 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             pick = pr.sel_wr();
         } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
             pick = pr.template sel_gi<GID>(alpha, beta);
-            sel += pr.last_coins;
+            msum += pr.last_coins;
         } else {
-            pick = pr.sel_gp(alpha);
-            sel += mt_ * (Vt - 2) * 4 * we;
-        }
-        // recount 12(V-1)W_E + substitution 8 W_E + selection
-        if (kCold) {
             if (tid == 0)
-                s_wops += 12 * (Vt - 1) * we + 8 * we + sel;
-        } else {
-            wops += 12 * (Vt - 1) * we + 8 * we + sel;
+                s_gpw += u64(pr.m) * u64(pr.V - 2) * 4 * u64(sd.words);
+            pick = pr.sel_gp(alpha);
         }
         const u32 q = pr.keys()[pick];
         pr.apply(q);  // a selected candidate always occurs (c >= 2)
@@ -2464,8 +2461,10 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             TCSE_REC[n_rec] = q;
         ++n_rec;
     }
-    if (kCold)
-        wops = s_wops;
+    {
+        const u64 S = u64(n_rec - n_rec0), we = u64(sd.words);
+        wops = we * (12 * (S * u64(V0 - 1) + S * (S - 1) / 2) + 8 * S) + msum + s_gpw;
+    }
 #undef TCSE_REC
 
     if (dump) {
