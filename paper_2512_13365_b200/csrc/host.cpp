@@ -369,7 +369,7 @@ void pick_bm(DevSys* d) {
     const int s0 = smem_one(*d);
     d->bm = true;
     const int s1 = smem_one(*d);
-    const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + 1024)); };
+    const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + kStaticSmem + 1024)); };
     d->bm = 4 * per_sm(s1) >= 3 * per_sm(s0);  // at most a quarter fewer resident processes
 }
 

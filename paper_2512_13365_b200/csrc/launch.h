@@ -239,7 +239,6 @@ struct Lay {
     u32 mask, keys0, cnts0;
     u32 tcnt, ncp, ncn, aux, newexcl, kcopy;                        // update view
     u32 qbase, wp, nA, nB, aoff, bs, cursor, alist, wbt, coin, bm;  // gi view
-    u32 mt, red, reds, redi, bcast;
     u32 coin_cap;  // coin bits of the gi view
     u32 total;     // bytes
 };
@@ -311,20 +310,17 @@ __host__ __device__ inline u32 carve(Lay* L, int W, int nt, int vcap, int mcap, 
     o += al16(u32(n_e + 2) * 8u);
     L->coin = o;
     L->coin_cap = u32(coin_words) * 32u;
-    o += al16(u32(coin_words) * 4u);
+    o += al16(u32(coin_words + 2) * 4u);  // + 2: the scoring windows read two words past a candidate's coins
     o = o > end_upd ? o : end_upd;
-    L->mt = o;
-    o += 312u * 8u;
-    L->red = o;
-    o += al16((NW + 2u) * 8u);
-    L->reds = o;
-    o += al16(NW * 16u);
-    L->redi = o;
-    o += al16(NW * 8u);
-    L->bcast = o;
-    o += 16u;
+    (void)NW;
     L->total = o;
     return o;
 }
+
+// static shared memory of a search block next to the carved dynamic part
+// (search.cu: the mt19937_64 state, reduction slots, broadcast words, the
+// layout itself and the kernel's per-process scalars), an upper bound for
+// occupancy estimates and the 227 KB limit
+constexpr int kStaticSmem = 4096;
 
 }  // namespace tcse

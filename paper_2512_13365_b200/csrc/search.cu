@@ -120,6 +120,16 @@ __device__ __forceinline__ double uniform_real(u64 x, double a, double b) {
 
 __shared__ Lay lay;
 
+// fixed-size per-process scratch at link-time addresses (static shared
+// memory, sized for the widest block): the process's mt19937_64 state, the
+// double-buffered block-reduction slots, the broadcast words.  Constant
+// addresses: no layout offset loaded from shared memory at each use.
+__shared__ u64 g_mt[312];
+__shared__ u32 g_red[2 * (8 + 2)];
+__shared__ double g_reds[2 * 8];
+__shared__ int g_redi[2 * 8];
+__shared__ u32 g_bcast[4];
+
 #if defined(TCSE_GI_STATS) || defined(TCSE_SNAP_STATS)
 // debug build only: gi path counters (approx steps, lone picks, folds,
 // overflow fallbacks, reference-loop steps, sum of m, multi-survivor steps)
@@ -285,8 +295,8 @@ __device__ __noinline__ void mt_seed(u64* mt, u64 s) {
 
 // the same seeding straight into the process's shared-memory state (one
 // thread; LDS/STS addressing)
-__device__ __noinline__ void mt_seed_smem(u32 off, u64 s) {
-    u64* mt = reinterpret_cast<u64*>(g_smem + off);
+__device__ __noinline__ void mt_seed_smem(u64 s) {
+    u64* mt = g_mt;
     u64 x = s;
     mt[0] = x;
 #pragma unroll 4
@@ -327,7 +337,7 @@ __device__ __forceinline__ u64 stream_seed(const SysDesc& sd, u64 seed) {
 template <int NT, bool COINS>
 __device__ __noinline__ void mt_twist_impl(u32* coin, u32 pos0, u32 n) {
     constexpr int R = (156 + NT - 1) / NT;
-    u64* mt = sp<u64>(lay.mt);
+    u64* mt = g_mt;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     u64 lo[R], hi[R];
@@ -377,7 +387,7 @@ __device__ __noinline__ void mt_twist_impl(u32* coin, u32 pos0, u32 n) {
 template <int NT>
 __device__ __noinline__ void mt_twist_small() {
     constexpr int R = (156 + NT - 1) / NT;
-    u64* mt = sp<u64>(lay.mt);
+    u64* mt = g_mt;
     const int tid = threadIdx.x;
     u64 v[R];
     __syncthreads();
@@ -430,7 +440,7 @@ __device__ __forceinline__ void coin_ballot(u32* coin, u32 pos0, int e, u32 n, u
 template <int NT>
 __device__ __noinline__ void mt_twist_small_coins(u32* coin, u32 pos0, u32 n) {
     constexpr int R = (156 + NT - 1) / NT;
-    u64* mt = sp<u64>(lay.mt);
+    u64* mt = g_mt;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     u64 v[R];
@@ -484,7 +494,7 @@ __device__ __noinline__ u32 mt_coin_run(u32* coin, u32 pos0, u32 nbits) {
     constexpr int NW = NT / 32;
     constexpr int RG = (5 + NW - 1) / NW;  // groups per warp
     __shared__ u64 bnd[2][12];             // per group (lo, hi) of lane 0, + lo of element 1
-    u64* mt = sp<u64>(lay.mt);
+    u64* mt = g_mt;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u64 lo[RG], hi[RG];
 #pragma unroll
@@ -685,7 +695,7 @@ __device__ __noinline__ int all_pairs(int V, int minc, u32* okeys, u16* ocnts, i
             local += count_pair<W>(a, a + 1 + (e >> 1), e & 1) >= minc ? 1u : 0u;
         u32 total;
         rsel ^= 1;
-        u32 ex = block_scan<NT>(local, sp<u32>(lay.red) + rsel * (NT / 32 + 2), &total);
+        u32 ex = block_scan<NT>(local, g_red + rsel * (NT / 32 + 2), &total);
         for (int e = e0; e < e1; ++e) {
             const int b = a + 1 + (e >> 1);
             const int cc = count_pair<W>(a, b, e & 1);
@@ -742,11 +752,11 @@ struct St {
     __device__ __forceinline__ u64* N(int v) { return mask_base() + size_t(v) * 2 * W + W; }
     __device__ __forceinline__ u32* red() {
         rsel ^= 1;
-        return sp<u32>(lay.red) + rsel * (NW + 2);
+        return g_red + rsel * (NW + 2);
     }
     __device__ __forceinline__ int argmax(double s, int idx) {
         rsel ^= 1;
-        const int q = block_argmax_double<NT>(s, idx, sp<double>(lay.reds) + rsel * NW, sp<int>(lay.redi) + rsel * NW);
+        const int q = block_argmax_double<NT>(s, idx, g_reds + rsel * NW, g_redi + rsel * NW);
         return q == 0x7fffffff ? 0 : q;  // only for NaN scores: stay inside the list
     }
 
@@ -756,7 +766,7 @@ struct St {
             mt_twist<NT>();
             mti = 0;
         }
-        return mt_temper(sp<u64>(lay.mt)[mti++]);
+        return mt_temper(g_mt[mti++]);
     }
 
     // uniform_int_distribution downscaling: _S_nd<unsigned __int128>
@@ -820,7 +830,7 @@ struct St {
             const u32 n = min(u32(312 - mti), nbits - done);
             const u32 sh = done & 31u;
             const u32 nw32 = (sh + n + 31) & ~31u;
-            const u64* mt = sp<u64>(lay.mt) + mti;
+            const u64* mt = g_mt + mti;
             u32* cw = coin + (done >> 5);
             for (u32 t = tid; t < nw32; t += NT) {
                 const u32 e = t - sh;  // wraps for t < sh: out of range
@@ -842,7 +852,7 @@ struct St {
     // ---- substitution (apply_substitution, linear_system.hpp:167-189):
     // returns the replaced occurrences; 0 leaves the state untouched
     __device__ int apply(u32 q) {
-        u32* bc = sp<u32>(lay.bcast);
+        u32* bc = g_bcast;
         if (tid == 0) {
             const int i = key_i(q) - 1, j = key_j(q) - 1, neg = key_neg(q);
             u64* pi = P(i);
@@ -1049,7 +1059,7 @@ struct St {
         const u64 sc_ex = block_scan_ool<NT>(local, red());
         u32 ex = u32(sc_ex);
         const u32 r = u32(nd(u32(sc_ex >> 32)));
-        u32* bc = sp<u32>(lay.bcast);
+        u32* bc = g_bcast;
 #pragma unroll 1
         for (int e = e0; e < e1; ++e)
             if (c[e] == mx) {
@@ -1064,7 +1074,7 @@ struct St {
     // weighted_random_from (85-98): first q with prefix(c - 1) > u * total
     __device__ int sel_wr() {
         const u16* c = cnts();
-        u32* bc = sp<u32>(lay.bcast);
+        u32* bc = g_bcast;
         // the total weight is the scan's total (one pass, two barriers less);
         // bc[1] was last read before the previous substitution's barriers
         if (tid == 0)
@@ -1325,13 +1335,14 @@ struct St {
             const u32 cap = lay.coin_cap;
             const u32 T = wp[m];
             const double eps =
-                ldexp(double(m + 16) * (double(*s_wmax) + fabs(alpha) * double(T) * fmax(1.0, beta)), -51);
+                double(m + 16) * (double(*s_wmax) + fabs(alpha) * double(T) * fmax(1.0, beta)) * 0x1p-51;
             const double eps2 = __dmul_rn(2.0, eps);
             double B = -INFINITY;  // running max of the approximate scores
             int q_lo = 0;
             while (q_lo < m) {
                 const u32 c0 = qbase[q_lo];
-                int lo = q_lo + 1, hi = m;
+                // (every remaining coin fits: the common case, no search)
+                int lo = qbase[m] - c0 <= cap ? m : q_lo + 1, hi = m;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (qbase[mid] - c0 <= cap)
@@ -1413,15 +1424,16 @@ struct St {
             const u32 cap = lay.coin_cap;
             const bool use_approx = approx && wp_total() < 65536u && *s_dmax <= 64u;
             const u32 T = use_approx ? wp_total() : 0u;
-            const double eps = use_approx ? ldexp(double(m + 16) * (double(*s_wmax) +
-                                                                    fabs(alpha) * double(T) * fmax(1.0, beta)), -51)
+            const double eps = use_approx ? double(m + 16) * (double(*s_wmax) +
+                                                              fabs(alpha) * double(T) * fmax(1.0, beta)) * 0x1p-51
                                           : 0.0;
             const double eps2 = __dmul_rn(2.0, eps);
             double B = -INFINITY;
             int q_lo = 0;
             while (q_lo < m) {
                 const u32 c0 = qbase[q_lo];
-                int lo = q_lo + 1, hi = m;
+                // (every remaining coin fits: the common case, no search)
+                int lo = qbase[m] - c0 <= cap ? m : q_lo + 1, hi = m;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (qbase[mid] - c0 <= cap)
@@ -1795,8 +1807,8 @@ struct St {
             return ((wi >> 24) << 16) | ((wi >> 16) & 0xffu);
         }
         rsel ^= 1;
-        double* r = sp<double>(lay.reds) + rsel * NW;
-        u32* ri = reinterpret_cast<u32*>(sp<int>(lay.redi) + rsel * NW);
+        double* r = g_reds + rsel * NW;
+        u32* ri = reinterpret_cast<u32*>(g_redi + rsel * NW);
         if (lane == 0) {
             r[tid >> 5] = wm;
             ri[tid >> 5] = wi;
@@ -2250,11 +2262,11 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
             // seed the process's mt19937_64 in shared memory (one thread, while
             // the others load the base state): no HBM hand-off
             if (tid == 0)
-                mt_seed_smem(lay.mt, stream_seed(sd, s_slot.seed));
+                mt_seed_smem(stream_seed(sd, s_slot.seed));
         } else if (s_slot.rng && tid < kCkpt) {
             // 32 checkpoints of the seeding chain (256 B from HBM per process):
             // lane c restarts the chain at word 10c and fills words 10c..10c+9
-            u64* mt = sp<u64>(lay.mt);
+            u64* mt = g_mt;
             u64 x = __ldg(L.rng + size_t(blk) * kCkpt + size_t(tid));
             const int i0 = tid * kCkptStride;
             mt[i0] = x;
