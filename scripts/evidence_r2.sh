@@ -11,6 +11,7 @@ timeout 600 python bench.py --config 0 > gpurun_out/${tag}_bench_cfg0.json 2> gp
 timeout 600 python bench.py --config 1 --steps 50 --warmup 5 > gpurun_out/${tag}_bench_cfg1.json 2> gpurun_out/${tag}_bench_cfg1.err
 timeout 600 python bench.py --config 3 > gpurun_out/${tag}_bench_cfg3.json 2> gpurun_out/${tag}_bench_cfg3.err
 timeout 900 python bench.py --config 4 --steps 2 --warmup 1 > gpurun_out/${tag}_bench_cfg4.json 2> gpurun_out/${tag}_bench_cfg4.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${tag}_ref_cfg2.json 2> gpurun_out/${tag}_ref_cfg2.err
 timeout 900 python bench.py --impl reference --config 3 > gpurun_out/${tag}_ref_cfg3.json 2> gpurun_out/${tag}_ref_cfg3.err
 timeout 1500 python bench.py --impl reference --config 4 --steps 2 --warmup 1 > gpurun_out/${tag}_ref_cfg4.json 2> gpurun_out/${tag}_ref_cfg4.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/${tag}_launches.csv \

@@ -37,7 +37,7 @@ for rep, out, what in [("%s_search.ncu-rep" % tag, "r02_%s_search_kernel_ncu.jso
     d = json.loads(run("scripts/ncu_summary.py", G(rep), note))
     d["what"] = what
     d["top_source_lines"] = run("scripts/ncu_lines.py", G(rep), "14").strip().split("\n")
-    d["regions"] = run("scripts/ncu_regions.py", G(rep)).strip().split("\n")[:16]
+    d["regions"] = run("scripts/ncu_regions.py", G(rep), *([os.environ["TCSE_PROFILED_SRC"]] if os.environ.get("TCSE_PROFILED_SRC") else [])).strip().split("\n")[:16]
     json.dump(d, open(P(out), "w"), indent=1)
     if "cfg" not in out:
         json.dump({"kernel": what, "dram_bytes_per_launch": nbytes(d["dram__bytes_read.sum"]) +
@@ -48,7 +48,7 @@ for c in range(5):
     src = G("%s_bench.json" % tag) if c == 2 else G("%s_bench_cfg%d.json" % (tag, c))
     if os.path.exists(src):
         shutil.copy(src, P("r02_bench_cfg%d.json" % c))
-for c in (3, 4):
+for c in (2, 3, 4):
     if os.path.exists(G("%s_ref_cfg%d.json" % (tag, c))):
         shutil.copy(G("%s_ref_cfg%d.json" % (tag, c)), P("r02_bench_reference_cfg%d.json" % c))
 if os.path.exists(G("%s_pipes.json" % tag)):
