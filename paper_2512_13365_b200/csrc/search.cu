@@ -830,18 +830,22 @@ struct St {
             const u32 n = min(u32(312 - mti), nbits - done);
             const u32 sh = done & 31u;
             const u32 nw32 = (sh + n + 31) & ~31u;
-            const u64* mt = g_mt + mti;
+            // (branch-free body: a clamped load from a 32-bit shared address
+            // computed once — a generic pointer makes the compiler rebuild
+            // the shared window base inside the loop —, one store path for
+            // lane 0; the loop bound is per warp)
+            const u32 mt_s = u32(__cvta_generic_to_shared(g_mt)) + 8u * u32(mti);
             u32* cw = coin + (done >> 5);
-            for (u32 t = tid; t < nw32; t += NT) {
-                const u32 e = t - sh;  // wraps for t < sh: out of range
-                const u32 bit = e < n ? coin_bit(mt[e]) : 0u;
-                const u32 ball = __ballot_sync(FULLMASK, bit);
-                if (lane == 0) {
-                    if (t < 32u && sh)
-                        cw[0] |= ball;
-                    else
-                        cw[t >> 5] = ball;
-                }
+            const u32 prev = sh ? cw[0] : 0u;  // the previous segment's bits of the first word
+            for (u32 t0 = u32(tid & ~31); t0 < nw32; t0 += NT) {
+                const u32 e = t0 + u32(lane) - sh;  // wraps for t < sh: out of range
+                const bool ok = e < n;
+                u32 lo, hi;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(mt_s + 8u * (ok ? e : 0u)));
+                const u32 bit = u32(__popc((hi & u32(kCoinMask >> 32)) ^ (lo & u32(kCoinMask)))) & 1u;
+                const u32 ball = __ballot_sync(FULLMASK, ok && bit);
+                if (lane == 0)
+                    cw[t0 >> 5] = t0 == 0u ? (prev | ball) : ball;
             }
             mti += int(n);
             done += n;
