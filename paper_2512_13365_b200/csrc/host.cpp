@@ -40,7 +40,7 @@
 #include "nccl_dyn.h"
 
 namespace tcse {
-cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st);
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, bool small, int smem, cudaStream_t st);
 struct ReduceLaunch;
 }  // namespace tcse
 
@@ -272,6 +272,7 @@ struct DevSys {
     int nt = 64;       // block size (threads per process)
     bool dense = true; // Greedy-Intersections form
     bool bm = false;   // dense layout with per-variable candidate bitmaps
+    bool small = false;  // the small-list instantiation (search.cu gi_dense_small)
     DBuf masks, keys, cnts;
     int base_m = 0;
     int mcap_full = 0;  // > 0: h.mcap was shrunk to the starting list + slack
@@ -357,6 +358,7 @@ int reg_blocks(int nt) { return nt == 32 ? 28 : (nt == 64 ? 14 : (nt == 128 ? 8 
 // TCSE_GI_BM=0/1 forces (results never depend on it).
 void pick_bm(DevSys* d) {
     d->bm = false;
+    d->small = false;
     if (!d->dense)
         return;
     const int forced = env_int("TCSE_GI_BM", -1);
@@ -364,13 +366,20 @@ void pick_bm(DevSys* d) {
         d->bm = forced != 0;
         return;
     }
-    if (env_int("TCSE_GI_PRUNE", d->base_m > 32 ? 1 : 0) == 0)
+    // without pruning the bitmaps serve lists of at most 32 candidates (the
+    // branch-free reference loop, search.cu gi_dense_small); TCSE_GI_SMALL=0
+    // keeps the plain loop there
+    static const int small = env_int("TCSE_GI_SMALL", 1);
+    const bool pruned = env_int("TCSE_GI_PRUNE", d->base_m > 32 ? 1 : 0) != 0;
+    const bool small_ok = small && !pruned && d->base_m <= 32 && d->W == 1 && d->nt == 32;
+    if (!pruned && !small_ok)
         return;
     const int s0 = smem_one(*d);
     d->bm = true;
     const int s1 = smem_one(*d);
     const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + kStaticSmem + 1024)); };
     d->bm = 4 * per_sm(s1) >= 3 * per_sm(s0);  // at most a quarter fewer resident processes
+    d->small = d->bm && small_ok;
 }
 
 // extra_vars: fresh variables a caller-supplied prefix may add beyond the
@@ -491,7 +500,7 @@ int run_dump(tcse_ctx* ctx, DevSys& d, const u32* d_prefix, int n_prefix, int mi
     if (prc)
         return prc;
     L.sys[0].gi_dense = d.dense;
-    CU(launch_search(L, d.W, d.nt, d.dense, smem_one(d), ctx->stream));
+    CU(launch_search(L, d.W, d.nt, d.dense, d.small, smem_one(d), ctx->stream));
     int rc = check_err(ctx);
     if (rc)
         return rc;
@@ -1015,7 +1024,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
         return rc;
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
     L.sys[0].gi_dense = d.dense;
-    CU(launch_search(L, d.W, d.nt, d.dense, smem_one(d), ctx->stream));
+    CU(launch_search(L, d.W, d.nt, d.dense, d.small, smem_one(d), ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
     rc = check_err(ctx);
     if (rc)

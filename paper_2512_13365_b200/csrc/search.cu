@@ -1106,7 +1106,7 @@ struct St {
     // select_greedy_intersections (162-176), alpha != 0.  Coins are drawn in
     // (q, s) order; q's score is the reference's sequential double sum,
     // evaluated in O(deg q) (see the header comment).
-    template <bool dense>
+    template <bool dense, bool SM = false>
     __device__ int sel_gi(double alpha, double beta) {
         // the walk needs a non-decreasing running sum (beta >= 0, always true
         // for assign_strategies' slots); any other beta runs the reference loop
@@ -1114,6 +1114,10 @@ struct St {
         // dense form with near-best pruning: integer score sums in the
         // candidate loop, exact folds only for near-ties (same bound as the walk)
         const bool approx = dense && gi_prune > 0 && m >= gi_prune && beta >= 0.0;
+        // lists of at most 32 candidates without pruning: the reference loop
+        // branch-free over bitmap neighbour masks (gi_dense_small)
+        // (its own instantiation, SM: the code costs the others spills)
+        const bool small = SM && dense && !approx && gi_bm && m <= 32;
         // max c - 1 over the list (crossing bound) and max coins per candidate
         // in wbt's spare slot
         u32* s_wmax = reinterpret_cast<u32*>(sp<double>(lay.wbt) + sd_ne + 1);
@@ -1136,7 +1140,7 @@ struct St {
             if (walk)
                 nB[v] = 0u;
         }
-        if (approx && gi_bm) {
+        if ((approx || small) && gi_bm) {
 #pragma unroll 1
             for (int v = tid; v < V1; v += NT)
 #pragma unroll 1
@@ -1158,7 +1162,7 @@ struct St {
             u32 lmax = 0u;
             // bitmap layout: row 0 (no variable has id 0) marks the heavy
             // candidates (c >= 3, weight > 1), one ballot per 32 of them
-            const bool hb = approx && gi_bm;
+            const bool hb = (approx || small) && gi_bm;
             const int mr = hb ? (m + 31) & ~31 : m;
 #pragma unroll 1
             for (int t = tid; t < mr; t += NT) {
@@ -1449,7 +1453,12 @@ struct St {
                 draw_coins(qbase[q_hi] - c0, dense && q_lo == 0);  // walk layout (beta < 0) clears here
                 if (!use_approx) {
                     GI_STAT(4, 1);
-                    const double2 r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
+                    double2 r;
+                    if constexpr (SM)
+                        r = small ? gi_dense_small(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q, int(bm_stride(mcap)))
+                                  : gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
+                    else
+                        r = gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
                     best_s = r.x;
                     best_q = __double_lo_as_int(r.y);
                 } else {
@@ -1586,6 +1595,40 @@ struct St {
             for (int t = 0; t < K; ++t)
                 if (qv[t] < q_hi)
                     gi_keep(__dadd_rn(double(int(c[qv[t]]) - 1), __dmul_rn(alpha, fut[t])), qv[t], best_s, best_q);
+        }
+        return make_double2(best_s, __int_as_double_lo(best_q));
+    }
+
+    // The same loop for lists of at most 32 candidates (m <= NT: one
+    // candidate per lane), branch-free: q's intersecting candidates as a
+    // 32-bit mask from the per-variable bitmaps, its coins as a 32-bit window
+    // in a register (deg q <= m - 1 <= 31).  The +0.0 additions of the reference (q
+    // itself, a coin that did not select) are skipped: exact, the running
+    // sum starts at +0.0 and never becomes -0.0.
+    static __device__ __noinline__ double2 gi_dense_small(const u32* ks, const u16* c, int m_, int q_lo, int q_hi,
+                                                          u32 c0, double alpha, double best_s, int best_q, int nwl) {
+        const int q = q_lo + int(threadIdx.x);
+        if (q < q_hi) {
+            const u32* bm = sp<u32>(lay.bm);
+            const double* wbt = sp<double>(lay.wbt);
+            const u32* coin = sp<u32>(lay.coin);
+            const u32 kq = ks[q];
+            const u32 nb = (bm[key_i(kq) * nwl] | bm[key_j(kq) * nwl]) & ~(1u << q);
+            const u32 p = sp<u32>(lay.qbase)[q] - c0;
+            u32 win = __funnelshift_r(coin[p >> 5], coin[(p >> 5) + 1], p & 31u);
+            double fut = 0.0;
+#pragma unroll 4
+            for (int s = 0; s < m_; ++s) {
+                const u16 cs = c[s];
+                const bool in = (nb >> s) & 1u;
+                if (!in && s != q)
+                    fut = __dadd_rn(fut, double(int(cs) - 1));
+                if (in && (win & 1u))
+                    fut = __dadd_rn(fut, wbt[cs]);
+                if (in)
+                    win >>= 1;
+            }
+            gi_keep(__dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, fut)), q, best_s, best_q);
         }
         return make_double2(best_s, __int_as_double_lo(best_q));
     }
@@ -2233,7 +2276,7 @@ __device__ __noinline__ void build_snapshots(const SysDesc& sd) {
     }
 }
 
-template <int W, int NT, bool GID>
+template <int W, int NT, bool GID, bool SM>
 __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const __grid_constant__ LaunchDesc L) {
     if (int(blockIdx.x) < L.n_builders) {
         build_snapshots<W, NT>(L.sys[blockIdx.x]);
@@ -2445,7 +2488,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         int pick;
 #if TCSE_ONLY_GI  // experiment: a Greedy-Intersections-only kernel (code size / registers)
         if (true) {
-            pick = pr.template sel_gi<GID>(alpha, beta);
+            pick = pr.template sel_gi<GID, SM>(alpha, beta);
             msum += pr.last_coins;
         } else
 #endif
@@ -2456,7 +2499,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const 
         } else if (strat == TCSE_WEIGHTED_RANDOM) {
             pick = pr.sel_wr();
         } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
-            pick = pr.template sel_gi<GID>(alpha, beta);
+            pick = pr.template sel_gi<GID, SM>(alpha, beta);
             msum += pr.last_coins;
         } else {
             if (tid == 0)
@@ -3220,9 +3263,9 @@ __global__ void __launch_bounds__(kTallyNT) flags_kernel(const __grid_constant__
 
 // ------------------------------------------------------------ dispatch
 
-template <int W, int NT, bool GID>
+template <int W, int NT, bool GID, bool SM = false>
 static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
-    auto k = search_kernel<W, NT, GID>;
+    auto k = search_kernel<W, NT, GID, SM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
@@ -3235,7 +3278,11 @@ static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
 
 // instantiated (W words, block size, gi form) combinations; the host picks
 // the block size with pick_nt() and the gi form by problem size
-cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
+cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, bool small, int smem, cudaStream_t st) {
+    // lists of at most 32 candidates (Laderman-size systems): their own
+    // one-warp instantiation with the branch-free gi loop (gi_dense_small)
+    if (small && dense && W == 1 && nt == 32)
+        return launch_w<1, 32, true, true>(L, smem, st);
 #define TCSE_CASE(w_, nt_)                                                                      \
     if (W == w_ && nt == nt_)                                                                   \
         return dense ? launch_w<w_, nt_, true>(L, smem, st) : launch_w<w_, nt_, false>(L, smem, st);
@@ -3255,7 +3302,7 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int 
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int smem, cudaStream_t st) {
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, bool small, int smem, cudaStream_t st) {
     const int g = (L.total_blocks + 127) / 128;
     if (L.hist) {
         cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * kHistStride * kMaxSys, st);
@@ -3268,7 +3315,7 @@ cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int sm
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
-    return launch_search_w(L, W, nt, dense, smem, st);
+    return launch_search_w(L, W, nt, dense, small, smem, st);
 }
 
 cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st) {
