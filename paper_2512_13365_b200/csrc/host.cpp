@@ -361,24 +361,24 @@ void pick_bm(DevSys* d) {
     d->small = false;
     if (!d->dense)
         return;
-    const int forced = env_int("TCSE_GI_BM", -1);
-    if (forced >= 0) {
-        d->bm = forced != 0;
-        return;
-    }
     // without pruning the bitmaps serve lists of at most 32 candidates (the
-    // branch-free reference loop, search.cu gi_dense_small); TCSE_GI_SMALL=0
-    // keeps the plain loop there
+    // branch-free reference loop in its own instantiation, search.cu
+    // gi_dense_small); TCSE_GI_SMALL=0 keeps the plain loop there
     static const int small = env_int("TCSE_GI_SMALL", 1);
     const bool pruned = env_int("TCSE_GI_PRUNE", d->base_m > 32 ? 1 : 0) != 0;
     const bool small_ok = small && !pruned && d->base_m <= 32 && d->W == 1 && d->nt == 32;
-    if (!pruned && !small_ok)
-        return;
-    const int s0 = smem_one(*d);
-    d->bm = true;
-    const int s1 = smem_one(*d);
-    const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + kStaticSmem + 1024)); };
-    d->bm = 4 * per_sm(s1) >= 3 * per_sm(s0);  // at most a quarter fewer resident processes
+    const int forced = env_int("TCSE_GI_BM", -1);
+    if (forced >= 0) {
+        d->bm = forced != 0;
+    } else {
+        if (!pruned && !small_ok)
+            return;
+        const int s0 = smem_one(*d);
+        d->bm = true;
+        const int s1 = smem_one(*d);
+        const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + kStaticSmem + 1024)); };
+        d->bm = 4 * per_sm(s1) >= 3 * per_sm(s0);  // at most a quarter fewer resident processes
+    }
     d->small = d->bm && small_ok;
 }
 

@@ -5,7 +5,8 @@ pruning (default: approximate scores from exact integer sums, exact folds only
 within the rounding bound of the best; dense: gi_score_bm or gi_pass, then
 gi_fold_dense) and
 without it (TCSE_GI_PRUNE=0: the walk folds every candidate, the dense layout
-runs the reference loop itself).
+runs the reference loop itself, branch-free over bitmaps for lists of at most
+32 candidates).
 
 The walk adds runs of disjoint candidates in O(1), including the binade
 crossings of the running double sum: by binary search below max(c-1)+1 and
@@ -60,20 +61,31 @@ def cyclic_system(n, offsets, copies):
 
 
 def systems(rng):
-    out = [random_system(rng, 40, 12) for _ in range(4)]
+    # small lists first (<= 32 candidates: the small-list instantiation)
+    out = [fixture_systems("laderman")[0], fixture_systems("laderman")[2], random_system(rng, 18, 8)]
+    out += [random_system(rng, 40, 12) for _ in range(4)]
     out += [cyclic_system(100, (0, 1, 3), 2), cyclic_system(64, (0, 1, 2, 5), 3)]
     out += [tall_system(rng, 90, 8, 0.45), tall_system(rng, 200, 9, 0.35), tall_system(rng, 250, 14, 0.2)]
     out += [fixture_systems("sxs")[2], fixture_systems("naive555_f1000")[2]]
     return out
 
 
-@pytest.mark.parametrize("form", ["1", "1-nobm", "1-exact", "0", "0-exact"])
-def test_gi_forms_match_oracle(dev, monkeypatch, form):
+def set_form(monkeypatch, form):
+    """form: '<dense>[-exact][-nobm|-plain]'.  Dense pruned scoring uses the
+    per-variable candidate bitmaps (gi_score_bm) or the full-list pass
+    (gi_pass, -nobm); dense without pruning (-exact) runs the reference loop —
+    branch-free over the bitmaps in the small-list instantiation for lists of
+    at most 32 candidates (gi_dense_small), the plain loop otherwise or with
+    -plain (TCSE_GI_SMALL=0)."""
     monkeypatch.setenv("TCSE_GI_DENSE", form[0])
-    monkeypatch.setenv("TCSE_GI_PRUNE", "0" if form.endswith("exact") else "1")
-    # dense pruned scoring: per-variable candidate bitmaps (gi_score_bm) or the
-    # full-list pass (gi_pass)
+    monkeypatch.setenv("TCSE_GI_PRUNE", "0" if "exact" in form else "1")
     monkeypatch.setenv("TCSE_GI_BM", "0" if form.endswith("nobm") else "1")
+    monkeypatch.setenv("TCSE_GI_SMALL", "0" if form.endswith("plain") else "1")
+
+
+@pytest.mark.parametrize("form", ["1", "1-nobm", "1-exact", "1-exact-plain", "0", "0-exact"])
+def test_gi_forms_match_oracle(dev, monkeypatch, form):
+    set_form(monkeypatch, form)
     rng = random.Random(4242)
     for sys_ in systems(rng):
         cfgs = gi_cfgs(rng, 18)
@@ -105,15 +117,13 @@ def test_negative_scores_gp(dev):
             assert (rec.substitutions, rec.cost) == o_run_cse(sys_, cfg), cfg
 
 
-@pytest.mark.parametrize("form", ["1", "1-nobm", "1-exact", "0"])
+@pytest.mark.parametrize("form", ["1", "1-nobm", "1-exact", "1-exact-plain", "0"])
 def test_gi_forms_many_coin_chunks(dev, monkeypatch, form):
     """A coin buffer of one candidate's worth (TCSE_COIN_MAX) splits every gi
     step into many chunks: chunk boundaries, the precleared first chunk and the
     per-chunk near-best folds must still reproduce the oracle."""
     monkeypatch.setenv("TCSE_COIN_MAX", "1")
-    monkeypatch.setenv("TCSE_GI_DENSE", form[0])
-    monkeypatch.setenv("TCSE_GI_PRUNE", "0" if form.endswith("exact") else "1")
-    monkeypatch.setenv("TCSE_GI_BM", "0" if form.endswith("nobm") else "1")
+    set_form(monkeypatch, form)
     rng = random.Random(777)
     for sys_ in systems(rng)[:8]:
         cfgs = gi_cfgs(rng, 12)
