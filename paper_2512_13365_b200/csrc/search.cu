@@ -1113,7 +1113,9 @@ struct St {
         const bool walk = !dense && beta >= 0.0;
         // dense form with near-best pruning: integer score sums in the
         // candidate loop, exact folds only for near-ties (same bound as the walk)
-        const bool approx = dense && gi_prune > 0 && m >= gi_prune && beta >= 0.0;
+        // (never in the small-list instantiation: its systems do not prune,
+        // so the pruning code is compiled out of it)
+        const bool approx = !SM && dense && gi_prune > 0 && m >= gi_prune && beta >= 0.0;
         // lists of at most 32 candidates without pruning: the reference loop
         // branch-free over bitmap neighbour masks (gi_dense_small)
         // (its own instantiation, SM: the code costs the others spills)
@@ -2114,9 +2116,13 @@ __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) 
 #ifndef TCSE_MINB64
 #define TCSE_MINB64 14
 #endif
-template <int NT>
+#ifndef TCSE_MINB_SMALL
+#define TCSE_MINB_SMALL TCSE_MINB32
+#endif
+template <int NT, bool SM = false>
 struct MinBlocks {
-    static constexpr int value = NT == 32 ? TCSE_MINB32 : (NT == 64 ? TCSE_MINB64 : (NT == 128 ? 8 : 4));
+    static constexpr int value =
+        SM ? TCSE_MINB_SMALL : (NT == 32 ? TCSE_MINB32 : (NT == 64 ? TCSE_MINB64 : (NT == 128 ? 8 : 4)));
 };
 
 // ------------------------------------------------------ prefix snapshots
@@ -2277,7 +2283,7 @@ __device__ __noinline__ void build_snapshots(const SysDesc& sd) {
 }
 
 template <int W, int NT, bool GID, bool SM>
-__global__ void __launch_bounds__(NT, MinBlocks<NT>::value) search_kernel(const __grid_constant__ LaunchDesc L) {
+__global__ void __launch_bounds__(NT, (MinBlocks<NT, SM>::value)) search_kernel(const __grid_constant__ LaunchDesc L) {
     if (int(blockIdx.x) < L.n_builders) {
         build_snapshots<W, NT>(L.sys[blockIdx.x]);
         return;
