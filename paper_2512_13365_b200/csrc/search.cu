@@ -1622,13 +1622,15 @@ struct St {
 #pragma unroll 4
             for (int s = 0; s < m_; ++s) {
                 const u16 cs = c[s];
-                const bool in = (nb >> s) & 1u;
-                if (!in && s != q)
-                    fut = __dadd_rn(fut, double(int(cs) - 1));
-                if (in && (win & 1u))
-                    fut = __dadd_rn(fut, wbt[cs]);
-                if (in)
-                    win >>= 1;
+                const u32 in = (nb >> s) & 1u;
+                // one addend and one predicated add (the compiler would add
+                // and select the result instead)
+                const u32 take = in ? (win & 1u) : u32(s != q);
+                const double a = in ? wbt[cs] : double(int(cs) - 1);
+                asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
+                    : "+d"(fut)
+                    : "d"(a), "r"(take));
+                win >>= in;
             }
             gi_keep(__dadd_rn(double(int(c[q]) - 1), __dmul_rn(alpha, fut)), q, best_s, best_q);
         }
