@@ -40,7 +40,7 @@
 #include "nccl_dyn.h"
 
 namespace tcse {
-cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, bool small, int smem, cudaStream_t st);
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int form, int smem, cudaStream_t st);
 struct ReduceLaunch;
 }  // namespace tcse
 
@@ -278,6 +278,9 @@ struct DevSys {
     int mcap_full = 0;  // > 0: h.mcap was shrunk to the starting list + slack
 };
 
+// the kernel form of a system's launch (search.cu kFormBm / kFormSmall)
+inline int kernel_form(const DevSys& d) { return (d.bm ? kFormBm : 0) | (d.small ? kFormSmall : 0); }
+
 namespace {
 
 int coin_words_for(const HostSys& h) {
@@ -352,6 +355,11 @@ int smem_one(const DevSys& d) {
 // processes per SM the register cap allows (search.cu MinBlocks)
 int reg_blocks(int nt) { return nt == 32 ? 28 : (nt == 64 ? 14 : (nt == 128 ? 8 : 4)); }
 
+// shapes with a bitmap-pruned instantiation (search.cu launch_search_w)
+bool bm_instantiated(int W, int nt) {
+    return (W == 1 && (nt == 32 || nt == 64 || nt == 128)) || (W == 2 && (nt == 64 || nt == 128));
+}
+
 // Per-variable candidate bitmaps (O(m/32 + deg) pruned gi scoring) whenever
 // the dense layout prunes and the bitmaps ((V+1) * ceil(mcap/32) words more
 // shared memory per process) cost at most a quarter of the resident processes.
@@ -359,7 +367,7 @@ int reg_blocks(int nt) { return nt == 32 ? 28 : (nt == 64 ? 14 : (nt == 128 ? 8 
 void pick_bm(DevSys* d) {
     d->bm = false;
     d->small = false;
-    if (!d->dense)
+    if (!d->dense || !bm_instantiated(d->W, d->nt))
         return;
     // without pruning the bitmaps serve lists of at most 32 candidates (the
     // branch-free reference loop in its own instantiation, search.cu
@@ -500,7 +508,7 @@ int run_dump(tcse_ctx* ctx, DevSys& d, const u32* d_prefix, int n_prefix, int mi
     if (prc)
         return prc;
     L.sys[0].gi_dense = d.dense;
-    CU(launch_search(L, d.W, d.nt, d.dense, d.small, smem_one(d), ctx->stream));
+    CU(launch_search(L, d.W, d.nt, d.dense, kernel_form(d), smem_one(d), ctx->stream));
     int rc = check_err(ctx);
     if (rc)
         return rc;
@@ -1024,7 +1032,7 @@ int tcse_run_cse(tcse_ctx* ctx, const tcse_system* sys, const tcse_pair* prefix,
         return rc;
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
     L.sys[0].gi_dense = d.dense;
-    CU(launch_search(L, d.W, d.nt, d.dense, d.small, smem_one(d), ctx->stream));
+    CU(launch_search(L, d.W, d.nt, d.dense, kernel_form(d), smem_one(d), ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
     rc = check_err(ctx);
     if (rc)

@@ -39,6 +39,13 @@ enum Mode : int32_t {
     kModeDump = 2     // replay prefix, dump pairs (count_pairs parity hook / base candidates)
 };
 
+// kernel forms (dense Greedy-Intersections layouts): the bitmap-pruned
+// scoring (gi_score_bm) and the small-list loop (gi_dense_small) are each
+// compiled only into the instantiations whose systems run them, so no
+// instantiation carries the others' code and registers
+constexpr int kFormBm = 1;     // per-variable candidate bitmaps (the system's gi_bm)
+constexpr int kFormSmall = 2;  // lists of at most 32 candidates, no pruning (bitmaps too)
+
 // device -> host only: a candidate list outgrew a shrunk session capacity
 // (the session re-runs the iteration at full capacity; never user-visible)
 constexpr int kErrCandOverflow = -100;

@@ -1106,8 +1106,10 @@ struct St {
     // select_greedy_intersections (162-176), alpha != 0.  Coins are drawn in
     // (q, s) order; q's score is the reference's sequential double sum,
     // evaluated in O(deg q) (see the header comment).
-    template <bool dense, bool SM = false>
+    template <bool dense, int F = 0>
     __device__ int sel_gi(double alpha, double beta) {
+        constexpr bool SM = (F & kFormSmall) != 0;
+        constexpr bool BM = (F & kFormBm) != 0;  // the system's gi_bm, known at compile time
         // the walk needs a non-decreasing running sum (beta >= 0, always true
         // for assign_strategies' slots); any other beta runs the reference loop
         const bool walk = !dense && beta >= 0.0;
@@ -1119,7 +1121,7 @@ struct St {
         // lists of at most 32 candidates without pruning: the reference loop
         // branch-free over bitmap neighbour masks (gi_dense_small)
         // (its own instantiation, SM: the code costs the others spills)
-        const bool small = SM && dense && !approx && gi_bm && m <= 32;
+        const bool small = SM && dense && !approx && m <= 32;
         // max c - 1 over the list (crossing bound) and max coins per candidate
         // in wbt's spare slot
         u32* s_wmax = reinterpret_cast<u32*>(sp<double>(lay.wbt) + sd_ne + 1);
@@ -1142,7 +1144,7 @@ struct St {
             if (walk)
                 nB[v] = 0u;
         }
-        if ((approx || small) && gi_bm) {
+        if (BM && (approx || small)) {
 #pragma unroll 1
             for (int v = tid; v < V1; v += NT)
 #pragma unroll 1
@@ -1164,7 +1166,7 @@ struct St {
             u32 lmax = 0u;
             // bitmap layout: row 0 (no variable has id 0) marks the heavy
             // candidates (c >= 3, weight > 1), one ballot per 32 of them
-            const bool hb = (approx || small) && gi_bm;
+            const bool hb = BM && (approx || small);
             const int mr = hb ? (m + 31) & ~31 : m;
 #pragma unroll 1
             for (int t = tid; t < mr; t += NT) {
@@ -1467,7 +1469,7 @@ struct St {
                     double lb = -INFINITY, h1 = 0.0, h2 = 0.0;
                     int q1 = -1, q2 = -1;
                     bool ovf = false;
-                    if (gi_bm) {
+                    if constexpr (BM) {
 #if TCSE_GI_BALANCE
                         // contiguous candidate ranges of equal work (coins + a
                         // per-candidate share) per thread: lanes finish together
@@ -2121,7 +2123,7 @@ __device__ __forceinline__ void set_error(const SysDesc& sd, int code, int pos) 
 #ifndef TCSE_MINB_SMALL
 #define TCSE_MINB_SMALL TCSE_MINB32
 #endif
-template <int NT, bool SM = false>
+template <int NT, bool SM>
 struct MinBlocks {
     static constexpr int value =
         SM ? TCSE_MINB_SMALL : (NT == 32 ? TCSE_MINB32 : (NT == 64 ? TCSE_MINB64 : (NT == 128 ? 8 : 4)));
@@ -2284,8 +2286,9 @@ __device__ __noinline__ void build_snapshots(const SysDesc& sd) {
     }
 }
 
-template <int W, int NT, bool GID, bool SM>
-__global__ void __launch_bounds__(NT, (MinBlocks<NT, SM>::value)) search_kernel(const __grid_constant__ LaunchDesc L) {
+template <int W, int NT, bool GID, int F>
+__global__ void __launch_bounds__(NT, (MinBlocks<NT, (F & kFormSmall) != 0>::value))
+    search_kernel(const __grid_constant__ LaunchDesc L) {
     if (int(blockIdx.x) < L.n_builders) {
         build_snapshots<W, NT>(L.sys[blockIdx.x]);
         return;
@@ -2496,7 +2499,7 @@ __global__ void __launch_bounds__(NT, (MinBlocks<NT, SM>::value)) search_kernel(
         int pick;
 #if TCSE_ONLY_GI  // experiment: a Greedy-Intersections-only kernel (code size / registers)
         if (true) {
-            pick = pr.template sel_gi<GID, SM>(alpha, beta);
+            pick = pr.template sel_gi<GID, F>(alpha, beta);
             msum += pr.last_coins;
         } else
 #endif
@@ -2507,7 +2510,7 @@ __global__ void __launch_bounds__(NT, (MinBlocks<NT, SM>::value)) search_kernel(
         } else if (strat == TCSE_WEIGHTED_RANDOM) {
             pick = pr.sel_wr();
         } else if (strat == TCSE_GREEDY_INTERSECTIONS) {
-            pick = pr.template sel_gi<GID, SM>(alpha, beta);
+            pick = pr.template sel_gi<GID, F>(alpha, beta);
             msum += pr.last_coins;
         } else {
             if (tid == 0)
@@ -3271,9 +3274,9 @@ __global__ void __launch_bounds__(kTallyNT) flags_kernel(const __grid_constant__
 
 // ------------------------------------------------------------ dispatch
 
-template <int W, int NT, bool GID, bool SM = false>
+template <int W, int NT, bool GID, int F = 0>
 static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
-    auto k = search_kernel<W, NT, GID, SM>;
+    auto k = search_kernel<W, NT, GID, F>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
@@ -3286,11 +3289,24 @@ static cudaError_t launch_w(const LaunchDesc& L, int smem, cudaStream_t st) {
 
 // instantiated (W words, block size, gi form) combinations; the host picks
 // the block size with pick_nt() and the gi form by problem size
-cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, bool small, int smem, cudaStream_t st) {
+cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int form, int smem, cudaStream_t st) {
     // lists of at most 32 candidates (Laderman-size systems): their own
     // one-warp instantiation with the branch-free gi loop (gi_dense_small)
-    if (small && dense && W == 1 && nt == 32)
-        return launch_w<1, 32, true, true>(L, smem, st);
+    if (dense && (form & kFormSmall) && W == 1 && nt == 32)
+        return launch_w<1, 32, true, kFormBm | kFormSmall>(L, smem, st);
+    // bitmap-pruned gi: the shapes host.cpp bm_instantiated() lists
+    if (dense && (form & kFormBm)) {
+        if (W == 1 && nt == 32)
+            return launch_w<1, 32, true, kFormBm>(L, smem, st);
+        if (W == 1 && nt == 64)
+            return launch_w<1, 64, true, kFormBm>(L, smem, st);
+        if (W == 2 && nt == 64)
+            return launch_w<2, 64, true, kFormBm>(L, smem, st);
+        if (W == 1 && nt == 128)
+            return launch_w<1, 128, true, kFormBm>(L, smem, st);
+        if (W == 2 && nt == 128)
+            return launch_w<2, 128, true, kFormBm>(L, smem, st);
+    }
 #define TCSE_CASE(w_, nt_)                                                                      \
     if (W == w_ && nt == nt_)                                                                   \
         return dense ? launch_w<w_, nt_, true>(L, smem, st) : launch_w<w_, nt_, false>(L, smem, st);
@@ -3310,7 +3326,7 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, bool
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, bool small, int smem, cudaStream_t st) {
+cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, int form, int smem, cudaStream_t st) {
     const int g = (L.total_blocks + 127) / 128;
     if (L.hist) {
         cudaError_t e = cudaMemsetAsync(L.hist, 0, sizeof(int32_t) * kHistStride * kMaxSys, st);
@@ -3323,7 +3339,7 @@ cudaError_t launch_search(const LaunchDesc& L, int W, int nt, bool dense, bool s
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return e;
-    return launch_search_w(L, W, nt, dense, small, smem, st);
+    return launch_search_w(L, W, nt, dense, form, smem, st);
 }
 
 cudaError_t launch_pack(const XchgLaunch& XL, cudaStream_t st) {
