@@ -273,6 +273,7 @@ struct DevSys {
     bool dense = true; // Greedy-Intersections form
     bool bm = false;   // dense layout with per-variable candidate bitmaps
     bool small = false;  // the small-list instantiation (search.cu gi_dense_small)
+    bool nt_auto = true; // block size chosen here (not forced by TCSE_NT)
     DBuf masks, keys, cnts;
     int base_m = 0;
     int mcap_full = 0;  // > 0: h.mcap was shrunk to the starting list + slack
@@ -320,10 +321,12 @@ void choose_launch(const tcse_ctx* ctx, DevSys* d) {
     d->W = launch_words(d->h.w_need);
     d->dense = gi_dense_for(d->h) != 0;
     int nt = ctx->nt;
+    d->nt_auto = nt == 0;
+    static const int nt64_max = env_int("TCSE_NT64_MAX", 1024);  // candidate capacity up to which two warps serve
     if (nt == 0) {
         if (d->W == 1 && d->h.mcap <= 96)
             nt = 32;  // one warp per process
-        else if (d->W <= 2 && d->h.mcap <= 1024)
+        else if (d->W <= 2 && d->h.mcap <= nt64_max)
             nt = 64;
         else if (d->h.mcap <= 1024)
             nt = 128;
@@ -345,6 +348,20 @@ void pick_form(DevSys* d) {
     if (env_int("TCSE_GI_DENSE", -1) < 0)
         d->dense = d->base_m <= dense_max;
     pick_bm(d);
+    // two warps denied their bitmaps by shared memory: four warps (half the
+    // resident processes by registers, so the bitmaps' shared memory costs
+    // relatively less) keep them — the bitmap scoring is worth more than the
+    // extra blocks (5x5x5 W: +19%; forced bitmaps at two warps +15%, four
+    // warps without them -12%).  TCSE_NT128_BM=0 disables.
+    static const int bm128 = env_int("TCSE_NT128_BM", 1);
+    if (bm128 && d->nt_auto && d->dense && !d->bm && d->nt == 64 && d->base_m > 32) {
+        d->nt = 128;
+        pick_bm(d);
+        if (!d->bm) {
+            d->nt = 64;
+            pick_bm(d);
+        }
+    }
 }
 
 int smem_one(const DevSys& d) {
