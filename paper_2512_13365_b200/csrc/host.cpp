@@ -17,6 +17,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <utility>
 #include <atomic>
 #include <condition_variable>
 #include <array>
@@ -341,27 +342,35 @@ void choose_launch(const tcse_ctx* ctx, DevSys* d) {
 // gi form on the actual starting list (lists only shrink): the dense
 // reference loop up to 512 candidates, the O(deg) walk beyond (sweep on every
 // fixture)
-void pick_bm(DevSys* d);
+void pick_bm(DevSys* d, int keep = 3);
+std::pair<int, int> bm_residency(DevSys* d);
+bool bm_instantiated(int W, int nt);
 
 void pick_form(DevSys* d) {
     static const int dense_max = env_int("TCSE_GI_DENSE_MAX", 512);
     if (env_int("TCSE_GI_DENSE", -1) < 0)
         d->dense = d->base_m <= dense_max;
     pick_bm(d);
-    // two warps denied their bitmaps by shared memory: four warps (half the
+    // two-warp systems whose bitmaps cost residency: four warps (half the
     // resident processes by registers, so the bitmaps' shared memory costs
-    // relatively less) keep them — the bitmap scoring is worth more than the
-    // extra blocks (5x5x5 W: +19%; forced bitmaps at two warps +15%, four
-    // warps without them -12%).  TCSE_NT128_BM=0 disables.
+    // relatively less) keep them at no more than a quarter — better than
+    // two warps with fewer blocks (5x5x5 W: +19% over two warps without
+    // bitmaps, +4% over two warps with them; four warps without them -12%).
+    // TCSE_NT128_BM=0 disables.
     static const int bm128 = env_int("TCSE_NT128_BM", 1);
-    if (bm128 && d->nt_auto && d->dense && !d->bm && d->nt == 64 && d->base_m > 32) {
+    if (bm128 && !d->bm && d->nt_auto && d->dense && d->nt == 64 && d->base_m > 32 &&
+        env_int("TCSE_GI_BM", -1) < 0 && bm_instantiated(d->W, 128)) {
         d->nt = 128;
         pick_bm(d);
-        if (!d->bm) {
+        if (!d->bm)
             d->nt = 64;
-            pick_bm(d);
-        }
     }
+    // still none: bitmaps worth up to half the resident processes (keep k =
+    // TCSE_BM_KEEP of 4) — the popcount scoring they enable outweighs the
+    // blocks (6x6x6 U/V at four warps: +3..5%)
+    static const int keep = env_int("TCSE_BM_KEEP", 2);
+    if (!d->bm && d->base_m > 32)
+        pick_bm(d, keep);
 }
 
 int smem_one(const DevSys& d) {
@@ -374,14 +383,28 @@ int reg_blocks(int nt) { return nt == 32 ? 28 : (nt == 64 ? 14 : (nt == 128 ? 8 
 
 // shapes with a bitmap-pruned instantiation (search.cu launch_search_w)
 bool bm_instantiated(int W, int nt) {
-    return (W == 1 && (nt == 32 || nt == 64 || nt == 128)) || (W == 2 && (nt == 64 || nt == 128));
+    return (W == 1 && (nt == 32 || nt == 64 || nt == 128)) || (W == 2 && (nt == 64 || nt == 128)) ||
+           ((W == 3 || W == 4) && nt == 128);
 }
 
 // Per-variable candidate bitmaps (O(m/32 + deg) pruned gi scoring) whenever
 // the dense layout prunes and the bitmaps ((V+1) * ceil(mcap/32) words more
 // shared memory per process) cost at most a quarter of the resident processes.
 // TCSE_GI_BM=0/1 forces (results never depend on it).
-void pick_bm(DevSys* d) {
+// resident processes per SM without and with the bitmaps at the system's
+// current block size
+std::pair<int, int> bm_residency(DevSys* d) {
+    const bool bm = d->bm;
+    d->bm = false;
+    const int s0 = smem_one(*d);
+    d->bm = true;
+    const int s1 = smem_one(*d);
+    d->bm = bm;
+    const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + kStaticSmem + 1024)); };
+    return {per_sm(s0), per_sm(s1)};
+}
+
+void pick_bm(DevSys* d, int keep) {
     d->bm = false;
     d->small = false;
     if (!d->dense || !bm_instantiated(d->W, d->nt))
@@ -398,11 +421,9 @@ void pick_bm(DevSys* d) {
     } else {
         if (!pruned && !small_ok)
             return;
-        const int s0 = smem_one(*d);
-        d->bm = true;
-        const int s1 = smem_one(*d);
-        const auto per_sm = [&](int s) { return std::min(reg_blocks(d->nt), (228 * 1024) / (s + kStaticSmem + 1024)); };
-        d->bm = 4 * per_sm(s1) >= 3 * per_sm(s0);  // at most a quarter fewer resident processes
+        // bitmaps if at least keep / 4 of the resident processes remain
+        const auto r = bm_residency(d);
+        d->bm = 4 * r.second >= keep * r.first;
     }
     d->small = d->bm && small_ok;
 }

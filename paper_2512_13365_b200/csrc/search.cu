@@ -3306,6 +3306,10 @@ cudaError_t launch_search_w(const LaunchDesc& L, int W, int nt, bool dense, int 
             return launch_w<1, 128, true, kFormBm>(L, smem, st);
         if (W == 2 && nt == 128)
             return launch_w<2, 128, true, kFormBm>(L, smem, st);
+        if (W == 3 && nt == 128)
+            return launch_w<3, 128, true, kFormBm>(L, smem, st);
+        if (W == 4 && nt == 128)
+            return launch_w<4, 128, true, kFormBm>(L, smem, st);
     }
 #define TCSE_CASE(w_, nt_)                                                                      \
     if (W == w_ && nt == nt_)                                                                   \
