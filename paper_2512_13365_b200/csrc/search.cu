@@ -1110,6 +1110,13 @@ struct St {
     __device__ int sel_gi(double alpha, double beta) {
         constexpr bool SM = (F & kFormSmall) != 0;
         constexpr bool BM = (F & kFormBm) != 0;  // the system's gi_bm, known at compile time
+#ifndef TCSE_GI_HYBRID
+#define TCSE_GI_HYBRID 1
+#endif
+        // one-warp pruned systems (the 4x4x4 U, V lists start at 40
+        // candidates): once the list is down to 32 the exact small-list loop
+        // replaces the approximate pass
+        constexpr bool HYB = TCSE_GI_HYBRID && BM && !SM && NT == 32;
         // the walk needs a non-decreasing running sum (beta >= 0, always true
         // for assign_strategies' slots); any other beta runs the reference loop
         const bool walk = !dense && beta >= 0.0;
@@ -1117,11 +1124,11 @@ struct St {
         // candidate loop, exact folds only for near-ties (same bound as the walk)
         // (never in the small-list instantiation: its systems do not prune,
         // so the pruning code is compiled out of it)
-        const bool approx = !SM && dense && gi_prune > 0 && m >= gi_prune && beta >= 0.0;
+        const bool approx = !SM && dense && gi_prune > 0 && m >= gi_prune && beta >= 0.0 && !(HYB && m <= 32);
         // lists of at most 32 candidates without pruning: the reference loop
         // branch-free over bitmap neighbour masks (gi_dense_small)
         // (its own instantiation, SM: the code costs the others spills)
-        const bool small = SM && dense && !approx && m <= 32;
+        const bool small = (SM || HYB) && dense && !approx && m <= 32;
         // max c - 1 over the list (crossing bound) and max coins per candidate
         // in wbt's spare slot
         u32* s_wmax = reinterpret_cast<u32*>(sp<double>(lay.wbt) + sd_ne + 1);
@@ -1458,7 +1465,7 @@ struct St {
                 if (!use_approx) {
                     GI_STAT(4, 1);
                     double2 r;
-                    if constexpr (SM)
+                    if constexpr (SM || HYB)
                         r = small ? gi_dense_small(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q, int(bm_stride(mcap)))
                                   : gi_dense_chunk(ks, c, m, q_lo, q_hi, c0, alpha, best_s, best_q);
                     else
