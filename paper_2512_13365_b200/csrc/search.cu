@@ -1116,7 +1116,9 @@ struct St {
         // one-warp pruned systems (the 4x4x4 U, V lists start at 40
         // candidates): once the list is down to 32 the exact small-list loop
         // replaces the approximate pass
-        constexpr bool HYB = TCSE_GI_HYBRID && BM && !SM && NT == 32;
+        // (also the 2-word two-warp kernel — 5x5x5 U, V lists start at ~40 —
+        // not the 1-word one: -2% on the 4x4x4 W group, +3.5% on 5x5x5:110)
+        constexpr bool HYB = TCSE_GI_HYBRID && BM && !SM && (NT == 32 || (NT == 64 && W == 2));
         // the walk needs a non-decreasing running sum (beta >= 0, always true
         // for assign_strategies' slots); any other beta runs the reference loop
         const bool walk = !dense && beta >= 0.0;
