@@ -626,7 +626,7 @@ __device__ __noinline__ void derive_slot(const SysDesc& sd, int iteration, u64 p
     const u64 l4 = x;
     x = kMtF * (x ^ (x >> 62)) + 5;
     const u64 l5 = x;
-#pragma unroll 1
+#pragma unroll 10
     for (u32 i = 6; i <= 156; ++i)
         x = kMtF * (x ^ (x >> 62)) + i;
     const u64 h0 = x;
@@ -2694,21 +2694,23 @@ __global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ L
         if (__syncthreads_or(o.seed)) {
             u64 x = o.ps;
             x0 = x;
-            int i = 0;
+            u64 x150 = 0;
+            // (the chain in unrolled 10-step segments between checkpoints:
+            // one thread per process at one warp per SM sub-partition, so
+            // the kernel's time is this chain's instruction count)
 #pragma unroll 1
             for (int r0 = 0; r0 < kCkpt; r0 += kSeedChunk) {
 #pragma unroll 1
                 for (int k = 0; k < kSeedChunk; ++k) {
-                    const int target = (r0 + k) * kCkptStride;
-#pragma unroll 1
-                    while (i < target) {
-                        ++i;
-                        x = kMtF * (x ^ (x >> 62)) + u64(i);
-                        if (i == 1)
-                            x1 = x;
-                        if (i == 156)
-                            x156 = x;
+                    const int c = r0 + k;  // checkpoint c = state word c * kCkptStride
+                    if (c > 0) {
+                        const u64 i0 = u64((c - 1) * kCkptStride);
+#pragma unroll
+                        for (int j = 1; j <= kCkptStride; ++j)
+                            x = kMtF * (x ^ (x >> 62)) + (i0 + u64(j));
                     }
+                    if (c == 15)
+                        x150 = x;
                     tile[tid][k] = x;
                 }
                 __syncthreads();
@@ -2721,6 +2723,12 @@ __global__ void __launch_bounds__(kPrepNT) prep_kernel(const __grid_constant__ L
                 }
                 __syncthreads();
             }
+            // state words 1 and 156 (the first output, work class below)
+            x1 = kMtF * (x0 ^ (x0 >> 62)) + 1ULL;
+            x156 = x150;
+#pragma unroll
+            for (int j = 151; j <= 156; ++j)
+                x156 = kMtF * (x156 ^ (x156 >> 62)) + u64(j);
         }
     }
     if (L.hist) {
